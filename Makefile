@@ -1,0 +1,30 @@
+# Build everything in-tree (the built .so files travel to the GPU box with the gpurun snapshot).
+#   make            -> paper_1910_00178_b200/lib/libngemm_cuda.so  (sm_100a only)
+#                      oracle/liboracle.so, oracle/_ref/libngemm_ref.so (test infrastructure)
+NVCC ?= /usr/local/cuda/bin/nvcc
+PKG := paper_1910_00178_b200
+CSRC := $(PKG)/csrc
+LIB := $(PKG)/lib/libngemm_cuda.so
+NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
+           -Xcompiler -fPIC -Xcompiler -Wall -shared -Iinclude -I$(CSRC) --expt-relaxed-constexpr
+
+all: $(LIB) oracle
+
+$(LIB): $(wildcard $(CSRC)/*.cu $(CSRC)/*.cuh) include/ngemm_cuda.h
+	mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -o $@ $(CSRC)/ngemm_cuda.cu -lcudart
+
+oracle:
+	$(MAKE) -s -C oracle
+
+ptxas:
+	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/ngemm_ptxas.so $(CSRC)/ngemm_cuda.cu 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" | head -80
+
+sass:
+	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > /tmp/ngemm.sass && grep -cE "UTCIMMA|UTMALDG|LDTM|IDP" /tmp/ngemm.sass
+
+clean:
+	rm -f $(LIB)
+	$(MAKE) -s -C oracle clean
+
+.PHONY: all oracle ptxas sass clean

@@ -1,0 +1,416 @@
+#!/usr/bin/env python3
+"""Benchmark: int8 GEMM TOPS (2*M*N*K/s) of C[i32] = A[u8] * B[i8]^T on B200 (BASELINE.json).
+
+Headline workload (the largest single-GPU config, BASELINE.json configs[4]):
+    c5  M = N = K = 16384, A uniform u8 [0,255], B uniform i8 [-128,127], exact int32
+        (WideningExact, gemm_ref semantics); A sharded by rows over the ranks, B replicated.
+A step = one pass of the hot path (one GEMM of this rank's row block).  Inputs are
+synthetic, drawn on the device with seeded torch generators (shapes and value
+distributions of the config); A+B = 512 MiB > L2, so every step streams from HBM.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config c5|c1|c2|c3|c4] [--mode exact|sat]
+
+Multi-GPU: launched under torch.distributed.run, one process per GPU (NCCL only for the
+barrier and the max-over-ranks of the timed region; the GEMM needs no collective).
+`--impl reference` times the reference's own CPU implementation (oracle/_ref: the
+unmodified header-only reference compiled from its sources; gemm_ref, the reference's only
+exact-mode kernel) on rank 0 with all host threads, on a bounded row sample of the same
+workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+SAT, EXACT = 0, 1
+INT8_PER_BF16 = 2.0  # int8 dense tensor rate = 2x bf16 (4.5 vs 2.25 PF nominal)
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=50)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="c5")
+    p.add_argument("--mode", choices=["exact", "sat"], default="exact")
+    p.add_argument("--shape", default=None, help="override MxNxK (sweeps)")
+    p.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt", "skinny"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    return p.parse_args()
+
+
+CONFIGS = {
+    "c1": (1024, 1024, 1024),
+    "c5": (16384, 16384, 16384),
+    "c4": (2048, 2048, 2048),
+}
+
+
+def workload(args):
+    if args.shape:
+        m, n, k = (int(x) for x in args.shape.lower().split("x"))
+        return f"custom {m}x{n}x{k}", m, n, k
+    if args.config in CONFIGS:
+        m, n, k = CONFIGS[args.config]
+        names = {"c1": "config1 single GEMM 1024^3", "c5": "config5 large GEMM 16384^3 (A row-sharded, B replicated)",
+                 "c4": "config4 2048^3"}
+        return names[args.config], m, n, k
+    raise SystemExit(f"unknown config {args.config} (use --shape MxNxK for c2/c3 shapes)")
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json)"
+    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """Polls NVML SM clocks and throttle reasons on a background thread during a region."""
+
+    REASONS = {0x8: "hw_slowdown", 0x40: "hw_thermal_slowdown", 0x20: "sw_thermal_slowdown", 0x4: "sw_power_cap",
+               0x80: "hw_power_brake_slowdown", 0x1: "gpu_idle", 0x2: "applications_clocks_setting"}
+
+    def __init__(self, index, period=0.01):
+        self.index, self.period = index, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nvml = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nvml = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nvml.nvmlDeviceGetClockInfo(self.h, self.nvml.NVML_CLOCK_SM))
+                r = self.nvml.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self.nvml:
+            self._t = threading.Thread(target=self._run, daemon=True)
+            self._t.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._t:
+            self._t.join()
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons), "samples": 0}
+        return {"sm_mhz": statistics.median(self.samples), "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def dist_setup(args):
+    import torch
+    import torch.distributed as dist
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(0)
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def sum_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return float(t.item())
+
+
+def load_traffic(tag):
+    """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary, if any."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            return json.load(f).get(tag)
+    except Exception:
+        return None
+
+
+def cpu_reference_sample(a_host, b_host, n, k, mode, target_s=12.0):
+    """The reference's own CPU path on a bounded row sample of the workload: the unmodified
+    reference compiled from its headers (oracle/_ref) when present, else our oracle port.
+    Returns (value_TOPS, cores, kind, sample_desc, seconds)."""
+    import numpy as np
+    from oracle.oracle import Oracle, Reference
+    threads = os.cpu_count() or 1
+    m_total = a_host.shape[0]
+    if Reference.available():
+        ref = Reference()
+        kind = "reference"
+        variant = "gemm_ref" if mode == EXACT else "gemm_conventional"
+
+        def run(rows):
+            s = ref.session(a_host[:rows], b_host, variant, mode, engine=0, threads=threads)
+            t0 = time.perf_counter()
+            s.run()
+            dt = time.perf_counter() - t0
+            s.close()
+            return dt
+        label = f"{variant} (oracle/_ref, host_isa={ref.host_isa_bits()} bit)"
+    else:
+        ora = Oracle()
+        kind = "port"
+
+        def run(rows):
+            t0 = time.perf_counter()
+            ora.gemm(a_host[:rows], b_host, mode, threads=threads)
+            return time.perf_counter() - t0
+        label = "oracle port (oracle/oracle.c)"
+    rows = min(m_total, threads)
+    dt = run(rows)
+    while dt < target_s / 4 and rows < m_total:
+        rows = min(m_total, max(rows + threads, int(rows * min(8.0, target_s / max(dt, 1e-3)))))
+        rows = max(threads, rows // threads * threads) if rows < m_total else m_total
+        dt = run(rows)
+    ops = 2.0 * rows * n * k
+    return ops / dt / 1e12, threads, kind, f"{label}: rows 0..{rows} of A ({rows}x{n}x{k}) against all of B, " \
+                                          f"{threads} threads, {dt:.2f} s", dt
+
+
+def run_ours(args):
+    import numpy as np
+    import torch
+    from paper_1910_00178_b200 import _lib, api
+
+    rank, world, local = dist_setup(args)
+    name, M, N, K = workload(args)
+    mode = EXACT if args.mode == "exact" else SAT
+    kernel = {"auto": _lib.KERNEL_AUTO, "tcgen05": _lib.KERNEL_TCGEN05, "simt": _lib.KERNEL_SIMT,
+              "skinny": _lib.KERNEL_SKINNY}[args.kernel]
+    rows = api.shard_rows(M, world, 128)
+    r0, r1 = rows[rank], rows[rank + 1]
+    mr = r1 - r0
+    dev = torch.device("cuda", local)
+
+    # synthetic inputs with the config's distributions, generated on the device
+    ga = torch.Generator(device=dev).manual_seed(0)
+    gb = torch.Generator(device=dev).manual_seed(1)
+    a_full_rows = torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32)
+    a = a_full_rows.to(torch.uint8)
+    del a_full_rows
+    b = torch.randint(-128, 128, (N, K), generator=gb, device=dev, dtype=torch.int32).to(torch.int8)
+    c = torch.empty((max(mr, 1), N), dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+    picked = _lib.KERNEL_NAMES[kernel] if kernel else api.pick_kernel(max(mr, 1), N, K, mode)
+
+    # small working sets: rotate distinct B/C buffers totalling > 4x L2 so every launch is L2-cold
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    per = (mr * K + N * K + 4 * mr * N)
+    nbuf = 1 if per > 2 * l2 else min(64, int((4 * l2) // max(per, 1)) + 1)
+    bs = [b] + [torch.randint(-128, 128, (N, K), generator=gb, device=dev, dtype=torch.int32).to(torch.int8)
+                for _ in range(nbuf - 1)]
+    as_ = [a] + [torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32).to(torch.uint8)
+                 for _ in range(nbuf - 1)]
+    cs = [c] + [torch.empty_like(c) for _ in range(nbuf - 1)]
+
+    def step(i):
+        if mr > 0:
+            api.gemm_device(as_[i % nbuf], bs[i % nbuf], cs[i % nbuf], mode=mode, kernel=kernel, stream=stream)
+
+    for i in range(args.warmup):
+        step(i)
+    torch.cuda.synchronize()
+    barrier(world)
+    torch.cuda.synchronize()
+
+    launches0 = _lib.launch_count()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        ev0.record(stream)
+        for i in range(args.steps):
+            step(i)
+        ev1.record(stream)
+        torch.cuda.synchronize()
+    launches = _lib.launch_count() - launches0
+    barrier(world)
+    torch.cuda.synchronize()
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, world)
+    ms_step = ms / args.steps
+    total_ops = 2.0 * M * N * K
+    value = total_ops / (ms_step * 1e-3) / 1e12  # TOPS, whole job
+
+    # dominant kernel: the GEMM itself (one launch per step); per-launch device time
+    kern_ms = ms_local / args.steps
+    hbm_gbs, bf16_tf, basis = measured_peaks()
+    alg_bytes = mr * K + N * K + 4 * mr * N
+    alg_ops = 2.0 * mr * N * K
+    tensor_bound = picked == "tcgen05" and (alg_ops / 4.5e15) > (alg_bytes / 8e12)
+    if tensor_bound:
+        peak = bf16_tf * INT8_PER_BF16
+        achieved = alg_ops / (kern_ms * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TOPS",
+                "frac": round(achieved / peak, 4),
+                "peak_basis": f"2 x bf16 dense tensor ({basis}: {bf16_tf} TF/s burst); datasheet 4500 TOPS",
+                "frac_of_datasheet": round(achieved / 4500.0, 4)}
+    else:
+        achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_gbs, "unit": "GB/s",
+                "frac": round(achieved / hbm_gbs, 4), "peak_basis": basis}
+    roof["traffic"] = load_traffic(f"{picked}:{mr}x{N}x{K}:{args.mode}")
+    roof["algorithmic_bytes_per_launch"] = alg_bytes
+    roof["algorithmic_ops_per_launch"] = alg_ops
+    roof["kernel"] = picked
+
+    # e2e through the reference-facing host entry (pinned host A/B -> device -> C host)
+    e2e = None
+    if not args.no_e2e and mr > 0:
+        L = _lib.load()
+        a_h = a.cpu().pin_memory()
+        b_h = b.cpu().pin_memory()
+        c_h = torch.empty((mr, N), dtype=torch.int32).pin_memory()
+        e_steps = max(2, min(args.steps, 5 if M * N * K >= 1 << 40 else args.steps))
+        for _ in range(min(2, args.warmup)):
+            _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_h.data_ptr(), b_h.data_ptr(), c_h.data_ptr(), mr, N, K, mode,
+                                                   kernel))
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_h.data_ptr(), b_h.data_ptr(), c_h.data_ptr(), mr, N, K, mode,
+                                                   kernel))
+        dt = (time.perf_counter() - t0) / e_steps
+        dt = max_over_ranks(dt, world)
+        e2e = {"value": round(total_ops / dt / 1e12, 3), "unit": "TOPS", "ms_per_step": round(dt * 1e3, 3),
+               "h2d_bytes_per_step": int(sum_over_ranks(mr * K + N * K, world)),
+               "d2h_bytes_per_step": int(sum_over_ranks(4 * mr * N, world)),
+               "path": "ngemm_cuda_gemm_u8i8_host (C-ABI, pinned host buffers, synchronous)"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        a_h = a.cpu().numpy()
+        b_h = b.cpu().numpy()
+        v, cores, kind, sample, _ = cpu_reference_sample(a_h, b_h, N, K, mode)
+        cpu = {"value": round(v, 5), "unit": "TOPS", "cores": cores, "kind": kind, "sample": sample}
+
+    if rank == 0:
+        line = {
+            "metric": "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T",
+            "value": round(value, 2), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "u8*s8->s32",
+            "data": "synthetic: A uniform u8 [0,255], B uniform i8 [-128,127] (torch generators seed 0/1, on device)",
+            "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode,
+                       "sat_semantics": "WideningExact (gemm_ref)" if mode == EXACT else
+                       "HardwareSaturating (gemm_sat_oracle)",
+                       "sharding": f"A rows over {world} rank(s), B replicated, no collective",
+                       "l2": "inputs larger than L2" if nbuf == 1 else f"{nbuf} rotating buffer sets > 4x L2"},
+            "kernel": picked, "gpu_launches": int(launches),
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    import numpy as np
+    from oracle.oracle import Oracle, Reference
+    name, M, N, K = workload(args)
+    mode = EXACT if args.mode == "exact" else SAT
+    ora = Oracle()
+    # same distributions as our arm (host-side seeded draws; the reference has its own PRNG)
+    rng = np.random.default_rng(0)
+    threads = os.cpu_count() or 1
+    # bounded sample: enough rows for ~3 s per step on all host threads
+    b = rng.integers(-128, 128, (N, K), dtype=np.int8)
+    a_probe = rng.integers(0, 256, (min(M, threads), K), dtype=np.uint8)
+    _, _, kind, _, dt = cpu_reference_sample(a_probe, b, N, K, mode, target_s=0.0)
+    rows = min(M, max(threads, int(threads * 3.0 / max(dt, 1e-3)) // threads * threads))
+    a = rng.integers(0, 256, (rows, K), dtype=np.uint8)
+    variant = "gemm_ref" if mode == EXACT else "gemm_conventional"
+    if Reference.available():
+        ref = Reference()
+        sess = ref.session(a, b, variant, mode, engine=0, threads=threads)
+        run = sess.run
+        label = f"{variant} (oracle/_ref unmodified reference, host_isa={ref.host_isa_bits()} bit)"
+    else:
+        run = lambda: ora.gemm(a, b, mode, threads=threads)  # noqa: E731
+        label = "oracle port (oracle/oracle.c)"
+    for _ in range(args.warmup):
+        run()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        run()
+    dt = (time.perf_counter() - t0) / args.steps
+    value = 2.0 * rows * N * K / dt / 1e12
+    sample = f"{label}: rows 0..{rows} of A ({rows}x{N}x{K}) against all of B per step, {threads} threads"
+    line = {
+        "impl": "reference",
+        "metric": "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T",
+        "value": round(value, 5), "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "u8*s8->s32", "data": "synthetic: A uniform u8 [0,255], B uniform i8 [-128,127] (numpy seed 0)",
+        "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode},
+        "cpu_baseline": {"value": round(value, 5), "unit": "TOPS", "cores": threads, "kind": kind, "sample": sample},
+        "e2e": {"value": round(value, 5), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,148 @@
+/*
+ * ngemm_cuda.h — the C-ABI drop-in boundary of the B200 u8 x i8 -> i32 GEMM engine
+ * (libngemm_cuda.so, hand-written sm_100a CUDA; no CPU fallback, no CUTLASS/cuBLAS).
+ *
+ * Plain pointers, sizes and status codes only.  Each entry point names the reference
+ * interface it replaces (paths under /root/reference/proj/include/ngemm):
+ *
+ *   reference                                                      -> this ABI
+ *   native::avx*_conv_u8i8_sat(a, b, c, m, n, k)                   -> ngemm_cuda_gemm_u8i8
+ *        (simd_native.hpp:144-147, 215-218; gemm.hpp:336-350)
+ *   native::avx*_ngemm_u8i8_sat(PackedWeight&, MatrixBuf&, C&)     -> ngemm_cuda_packed_upload +
+ *        (simd_native.hpp:282-283, 361-363; gemm.hpp:385-395)          ngemm_cuda_gemm_packed
+ *   detail::emu_conv_u8i8 / emu_ngemm_u8i8 (Engine::Emulated)       -> kernel NGEMM_KERNEL_SIMT
+ *        (gemm.hpp:113-159, 192-243)
+ *   gemm_conventional / gemm_ngemm on host MatrixBufs               -> ngemm_cuda_gemm_u8i8_host /
+ *        (gemm.hpp:327-369, 373-409)                                   ngemm_cuda_gemm_packed_host
+ *   PackedWeight::block_offset inverse (layout.hpp:152-171)         -> ngemm_cuda_repack
+ *
+ * Semantics (bit-exact):
+ *   sat_mode 1 (WideningExact):      C[m][n] = sum_k A[m][k]*B[n][k]  mod 2^32   (gemm.hpp:36-52)
+ *   sat_mode 0 (HardwareSaturating): C[m][n] = sum_j sat16(A[m][2j]B[n][2j] + A[m][2j+1]B[n][2j+1])
+ *                                    mod 2^32, odd K tail paired with 0     (gemm.hpp:83-104)
+ *   (0/1 follow the reference enum order, lanes.hpp:18.)
+ *
+ * Conventions: A is [M x K] u8 row-major (row stride lda bytes), B is [N x K] i8 row-major
+ * (ldb), C is [M x N] i32 row-major (ldc elements).  C is fully overwritten (no zero-init
+ * needed).  Errors are reported before any launch and map 1:1 to the reference exception
+ * types (common.hpp:77-127).  Device-pointer entries are asynchronous on `stream`
+ * (a cudaStream_t, NULL = legacy default stream) and reentrant per stream.
+ */
+#ifndef NGEMM_CUDA_H
+#define NGEMM_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define NGEMM_CUDA_ABI_VERSION 1
+
+typedef enum {
+    NGEMM_OK = 0,
+    NGEMM_ERR_SHAPE = 1,       /* ShapeError        (common.hpp:82-85) */
+    NGEMM_ERR_UNSUPPORTED = 2, /* UnsupportedError  (common.hpp:114-117) */
+    NGEMM_ERR_CONFIG = 3,      /* ConfigError       (common.hpp:104-107) */
+    NGEMM_ERR_RANGE = 4,       /* RangeError        (common.hpp:87-90) */
+    NGEMM_ERR_CORRUPTION = 5,  /* CorruptionError   (common.hpp:109-112) */
+    NGEMM_ERR_INDEX = 6,       /* IndexError        (common.hpp:92-95) */
+    NGEMM_ERR_CUDA = 7         /* CUDA runtime failure (Error base class) */
+} ngemm_status;
+
+typedef enum {
+    NGEMM_SAT_HARDWARE = 0, /* SatMode::HardwareSaturating */
+    NGEMM_SAT_EXACT = 1     /* SatMode::WideningExact */
+} ngemm_sat_mode;
+
+/* Kernel selection; AUTO is what every reference-facing entry uses. */
+typedef enum {
+    NGEMM_KERNEL_AUTO = 0,
+    NGEMM_KERNEL_TCGEN05 = 1, /* tensor-core tcgen05.mma kind::i8 (exact mode; sat mode only when
+                                 the inputs provably cannot saturate) */
+    NGEMM_KERNEL_SIMT = 2,    /* CUDA-core dp4a tiled kernel, both modes (the Engine::Emulated path) */
+    NGEMM_KERNEL_SKINNY = 3   /* memory-bound M <= 16 path, both modes */
+} ngemm_kernel;
+
+/* PackedWeight metadata (layout.hpp:120-135; NGPT trailer layout.hpp:283-293). */
+typedef struct {
+    int32_t w, h, v;      /* KernelShape */
+    int64_t tm, tn, tk;   /* TileConfig */
+    int32_t perm;         /* Perm tag 0..5 = MNK MKN NMK NKM KMN KNM (layout.hpp:54) */
+    int64_t m_orig, k_orig;
+    int64_t m_pad, k_pad; /* must equal round_up(m_orig, tm), round_up(k_orig, tk) */
+} ngemm_packed_meta;
+
+/* Opaque device-resident prepacked weight: the K-major, 16-byte-stride copy of A that the
+ * kernels consume, made once per weight (the paper's offline prepack). */
+typedef struct ngemm_packed_dev* ngemm_packed_handle;
+
+/* ---- device-pointer entries ------------------------------------------------------------ */
+
+/* C = A * B^T on device pointers (replaces avx*_conv_u8i8_sat). */
+ngemm_status ngemm_cuda_gemm_u8i8(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
+                                  int32_t* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
+                                  int sat_mode, void* stream);
+
+/* Same, forcing one kernel (tests / bench / ncu evidence per kernel choice). */
+ngemm_status ngemm_cuda_gemm_u8i8_ex(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
+                                     int32_t* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
+                                     int sat_mode, int kernel, void* stream);
+
+/* Device repack: packed bytes (d_packed, m_pad*k_pad) -> row-major A (m_orig x k_orig, row
+ * stride lda >= k_orig) on `stream`.  Inverse of PackedWeight::elem_offset. */
+ngemm_status ngemm_cuda_repack(const ngemm_packed_meta* meta, const uint8_t* d_packed, uint8_t* d_a,
+                               int64_t lda, void* stream);
+
+/* Validates the metadata like TileConfig::validate / pack_weights (layout.hpp:92-102, 258-263). */
+ngemm_status ngemm_cuda_packed_validate(const ngemm_packed_meta* meta);
+
+/* Upload host packed bytes to the current device and repack to the device-resident layout. */
+ngemm_status ngemm_cuda_packed_upload(const ngemm_packed_meta* meta, const uint8_t* host_packed,
+                                      size_t nbytes, ngemm_packed_handle* out);
+/* Build a handle from an already device-resident row-major A (device copy is made). */
+ngemm_status ngemm_cuda_packed_from_device(const uint8_t* d_a, int64_t lda, int64_t m, int64_t k,
+                                           ngemm_packed_handle* out);
+ngemm_status ngemm_cuda_packed_free(ngemm_packed_handle h);
+/* Device pointer / row stride of the handle's K-major A (for custom launches). */
+ngemm_status ngemm_cuda_packed_info(ngemm_packed_handle h, const uint8_t** d_a, int64_t* lda,
+                                    int64_t* m, int64_t* k, int* device);
+
+/* C = unpack(P) * B^T with a device-resident handle (replaces avx*_ngemm_u8i8_sat). */
+ngemm_status ngemm_cuda_gemm_packed(ngemm_packed_handle h, const int8_t* b, int64_t ldb, int32_t* c,
+                                    int64_t ldc, int64_t n, int sat_mode, void* stream);
+
+/* ---- host-pointer entries (synchronous; what the C++ drop-in headers call) -------------- */
+
+ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_t* c, int64_t m,
+                                       int64_t n, int64_t k, int sat_mode, int kernel);
+ngemm_status ngemm_cuda_gemm_packed_host(const ngemm_packed_meta* meta, const uint8_t* host_packed,
+                                         size_t nbytes, const int8_t* b, int32_t* c, int64_t n,
+                                         int sat_mode, int kernel);
+
+/* ---- multi-GPU M-shard driver (single process, one stream per device) -------------------
+ * A's rows are split into ndev contiguous, tile-aligned blocks; B is replicated; device d
+ * writes rows [row_start[d], row_start[d+1]) of C.  Host pointers; if gather_device >= 0
+ * the full C is also assembled on that device (peer copies over NVLink) and returned in
+ * *gathered (caller frees with ngemm_cuda_free). */
+ngemm_status ngemm_cuda_shard_rows(int64_t m, int ndev, int64_t align, int64_t* row_start /* ndev+1 */);
+ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint8_t* a, const int8_t* b,
+                                        int32_t* c, int64_t m, int64_t n, int64_t k, int sat_mode,
+                                        int gather_device, int32_t** gathered);
+ngemm_status ngemm_cuda_free(void* device_ptr);
+
+/* ---- introspection ----------------------------------------------------------------------- */
+int ngemm_cuda_abi_version(void);
+const char* ngemm_cuda_status_name(int status);
+/* Thread-local message of the last failing call on this thread ("" if none). */
+const char* ngemm_cuda_last_error(void);
+/* Kernel AUTO would pick for a shape (NGEMM_KERNEL_*), without launching. */
+int ngemm_cuda_pick_kernel(int64_t m, int64_t n, int64_t k, int sat_mode);
+/* Number of kernels this library launched since load (all entries, all threads). */
+uint64_t ngemm_cuda_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* NGEMM_CUDA_H */

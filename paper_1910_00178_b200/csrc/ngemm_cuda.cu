@@ -1,0 +1,608 @@
+// ngemm_cuda.cu — the C-ABI (include/ngemm_cuda.h) over the hand-written sm_100a kernels.
+//
+// Validation happens before any launch and maps 1:1 onto the reference exception types
+// (gemm.hpp:19-30, 375-382; layout.hpp:92-102, 254-263).  There is no CPU path: if the
+// device or the sm_100a image is missing, every entry returns NGEMM_ERR_CUDA.
+#include "ngemm_cuda.h"
+
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "kernel_layout.cuh"
+#include "kernel_simt.cuh"
+#include "kernel_skinny.cuh"
+#include "kernel_tcgen05.cuh"
+
+using namespace ngemm_dev;
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<uint64_t> g_launches{0};
+
+ngemm_status fail(ngemm_status s, const std::string& msg) {
+    g_last_error = msg;
+    return s;
+}
+
+#define NG_CUDA(expr)                                                                              \
+    do {                                                                                           \
+        cudaError_t e_ = (expr);                                                                   \
+        if (e_ != cudaSuccess)                                                                     \
+            return fail(NGEMM_ERR_CUDA, std::string(#expr) + ": " + cudaGetErrorString(e_));       \
+    } while (0)
+
+#define NG_LAUNCHED()                                                                              \
+    do {                                                                                           \
+        cudaError_t e_ = cudaGetLastError();                                                       \
+        if (e_ != cudaSuccess) return fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                                        \
+    } while (0)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct DevInfo {
+    int sms = 0;
+    int smem_optin = 0;
+    int cc_major = 0, cc_minor = 0;
+};
+
+DevInfo dev_info(int dev) {
+    static std::mutex mu;
+    static DevInfo cache[64];
+    static bool have[64] = {};
+    std::lock_guard<std::mutex> lk(mu);
+    if (dev >= 0 && dev < 64 && have[dev]) return cache[dev];
+    DevInfo d;
+    cudaDeviceGetAttribute(&d.sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&d.smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+    cudaDeviceGetAttribute(&d.cc_major, cudaDevAttrComputeCapabilityMajor, dev);
+    cudaDeviceGetAttribute(&d.cc_minor, cudaDevAttrComputeCapabilityMinor, dev);
+    if (dev >= 0 && dev < 64 && d.sms > 0) {
+        cache[dev] = d;
+        have[dev] = true;
+    }
+    return d;
+}
+
+ngemm_status current_device(int* dev, DevInfo* info) {
+    NG_CUDA(cudaGetDevice(dev));
+    *info = dev_info(*dev);
+    if (info->sms <= 0) return fail(NGEMM_ERR_CUDA, "no CUDA device");
+    if (info->cc_major != 10 || info->cc_minor != 0)
+        return fail(NGEMM_ERR_UNSUPPORTED, "libngemm_cuda is built for sm_100a (B200); device is sm_" +
+                                               std::to_string(info->cc_major) + std::to_string(info->cc_minor));
+    return NGEMM_OK;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+using EncodeTiledFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                   const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+    static EncodeTiledFn fn = [] {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPointByVersion("cuTensorMapEncodeTiled", &p, 12000, cudaEnableDefault, &q) !=
+                cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            return static_cast<EncodeTiledFn>(nullptr);
+        return reinterpret_cast<EncodeTiledFn>(p);
+    }();
+    return fn;
+}
+
+// 2-D u8 tensor [outer x inner] with row stride `stride` bytes, box [box_outer x box_inner],
+// SWIZZLE_128B, out-of-bounds elements read as zero.
+ngemm_status make_tmap_u8(CUtensorMap* map, const void* base, uint64_t inner, uint64_t outer, uint64_t stride,
+                          uint32_t box_inner, uint32_t box_outer) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(NGEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {inner, outer};
+    cuuint64_t strides[1] = {stride};
+    cuuint32_t box[2] = {box_inner, box_outer};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void*>(base), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(NGEMM_ERR_CUDA, "cuTensorMapEncodeTiled failed: " + std::to_string(r));
+    return NGEMM_OK;
+}
+
+bool tma_ok(const void* p, int64_t ld) {
+    return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 16 == 0 && ld < (int64_t(1) << 39);
+}
+
+// ---------------------------------------------------------------- validation
+ngemm_status validate(const void* a, int64_t lda, const void* b, int64_t ldb, const void* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, int mode) {
+    if (mode != NGEMM_SAT_HARDWARE && mode != NGEMM_SAT_EXACT)
+        return fail(NGEMM_ERR_CONFIG, "sat_mode must be 0 (HardwareSaturating) or 1 (WideningExact)");
+    if (m < 1 || n < 1 || k < 1)
+        return fail(NGEMM_ERR_SHAPE, "gemm: dims must be >= 1, got " + std::to_string(m) + "x" + std::to_string(n) +
+                                         "x" + std::to_string(k));
+    if (lda < k || ldb < k || ldc < n) return fail(NGEMM_ERR_SHAPE, "gemm: leading dimension smaller than the row");
+    if (!a || !b || !c) return fail(NGEMM_ERR_SHAPE, "gemm: null operand");
+    if (m > INT32_MAX / 2 || n > INT32_MAX / 2) return fail(NGEMM_ERR_SHAPE, "gemm: dimension too large");
+    return NGEMM_OK;
+}
+
+// ---------------------------------------------------------------- launchers
+template <typename K>
+ngemm_status set_smem(K kernel, int bytes) {
+    NG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return NGEMM_OK;
+}
+
+ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st) {
+    const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
+                        lda % 16 == 0 && ldb % 16 == 0);
+    const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
+    dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
+    if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
+    if (mode == NGEMM_SAT_EXACT)
+        simt_gemm_kernel<1><<<grid, simt::THREADS, 0, st>>>(a, lda, b, ldb, c, ldc, m, n, k, vec_ok, c_vec);
+    else
+        simt_gemm_kernel<0><<<grid, simt::THREADS, 0, st>>>(a, lda, b, ldb, c, ldc, m, n, k, vec_ok, c_vec);
+    NG_LAUNCHED();
+    return NGEMM_OK;
+}
+
+constexpr int kSkinnyMaxM = 16;
+constexpr int64_t kSkinnySmemCap = 200 * 1024;
+
+bool skinny_fits(int64_t m, int64_t k) {
+    int mt = 1;
+    while (mt < m) mt *= 2;
+    return m <= kSkinnyMaxM && mt * round_up(k, 16) <= kSkinnySmemCap;
+}
+
+template <int MODE, int MT, int NR>
+ngemm_status launch_skinny_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                             int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    const int64_t kpad = round_up(k, 16);
+    const int smem = static_cast<int>(MT * kpad);
+    auto kern = skinny_gemm_kernel<MODE, MT, NR>;
+    if (smem > 48 * 1024) {
+        ngemm_status s = set_smem(kern, smem);
+        if (s != NGEMM_OK) return s;
+    }
+    const int b_vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0);
+    const int64_t groups = (n + NR - 1) / NR;
+    int64_t blocks = (groups + skinny::WARPS - 1) / skinny::WARPS;
+    blocks = std::min<int64_t>(blocks, static_cast<int64_t>(di.sms) * 8);
+    kern<<<static_cast<unsigned>(blocks), skinny::THREADS, smem, st>>>(a, lda, b, ldb, c, ldc, static_cast<int>(m), n,
+                                                                      k, kpad, b_vec);
+    NG_LAUNCHED();
+    return NGEMM_OK;
+}
+
+template <int MODE>
+ngemm_status launch_skinny_mode(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    if (m <= 1) return launch_skinny_t<MODE, 1, 8>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m <= 2) return launch_skinny_t<MODE, 2, 8>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m <= 4) return launch_skinny_t<MODE, 4, 4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m <= 8) return launch_skinny_t<MODE, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    return launch_skinny_t<MODE, 16, 4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+}
+
+ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                           int64_t m, int64_t n, int64_t k, int mode, const DevInfo& di, cudaStream_t st) {
+    if (!skinny_fits(m, k)) return fail(NGEMM_ERR_UNSUPPORTED, "skinny path needs M <= 16 and A resident in smem");
+    return mode == NGEMM_SAT_EXACT ? launch_skinny_mode<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
+                                   : launch_skinny_mode<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+}
+
+template <int BN, int STAGES>
+ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, int32_t* c, int64_t ldc, int64_t m,
+                         int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    using S = tc::Smem<BN, STAGES>;
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ngemm_status s = NGEMM_OK;
+    std::call_once(once[dev & 63], [&] { s = set_smem(tc_gemm_kernel<BN, STAGES>, S::TOTAL); });
+    if (s != NGEMM_OK) return s;
+    TileMap map;
+    map.tiles_m = static_cast<int>((m + tc::BM - 1) / tc::BM);
+    map.tiles_n = static_cast<int>((n + BN - 1) / BN);
+    const int num_kb = static_cast<int>((k + tc::BK - 1) / tc::BK);
+    const int tiles = map.tiles_m * map.tiles_n;
+    int splits = 1;
+    if (tiles * 2 <= di.sms && num_kb >= 8) splits = std::max(1, std::min(num_kb / 4, di.sms / tiles));
+    map.splits = splits;
+    if (splits > 1) {
+        if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
+        else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
+    }
+    const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
+    const int grid = std::min(tiles * splits, di.sms);
+    tc_gemm_kernel<BN, STAGES><<<grid, tc::THREADS, S::TOTAL, st>>>(ta, tb, c, ldc, static_cast<int>(m),
+                                                                   static_cast<int>(n), num_kb, map, c_vec);
+    NG_LAUNCHED();
+    return NGEMM_OK;
+}
+
+ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                            int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3): stage ragged
+    // operands through a zero-padded scratch copy (padding K at the end is neutral).
+    const uint8_t* a_use = a;
+    const uint8_t* b_use = reinterpret_cast<const uint8_t*>(b);
+    int64_t lda_use = lda, ldb_use = ldb;
+    uint8_t* scratch = nullptr;
+    if (!tma_ok(a, lda) || !tma_ok(b, ldb)) {
+        const int64_t kp = round_up(k, 16);
+        const size_t bytes = static_cast<size_t>((tma_ok(a, lda) ? 0 : m * kp) + (tma_ok(b, ldb) ? 0 : n * kp));
+        NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st));
+        uint8_t* p = scratch;
+        if (!tma_ok(a, lda)) {
+            NG_CUDA(cudaMemcpy2DAsync(p, kp, a, lda, k, m, cudaMemcpyDeviceToDevice, st));
+            a_use = p;
+            lda_use = kp;
+            p += m * kp;
+        }
+        if (!tma_ok(b, ldb)) {
+            NG_CUDA(cudaMemcpy2DAsync(p, kp, b, ldb, k, n, cudaMemcpyDeviceToDevice, st));
+            b_use = p;
+            ldb_use = kp;
+        }
+    }
+    const int bn = (n <= 128) ? 128 : 256;
+    CUtensorMap ta, tb;
+    ngemm_status s = make_tmap_u8(&ta, a_use, k, m, lda_use, tc::BK, tc::BM);
+    if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, bn);
+    if (s == NGEMM_OK)
+        s = bn == 128 ? launch_tc_t<128, 6>(ta, tb, c, ldc, m, n, k, di, st)
+                      : launch_tc_t<256, 4>(ta, tb, c, ldc, m, n, k, di, st);
+    if (scratch) cudaFreeAsync(scratch, st);
+    return s;
+}
+
+int pick(int64_t m, int64_t n, int64_t k, int mode) {
+    (void)n;
+    if (m <= kSkinnyMaxM && skinny_fits(m, k)) return NGEMM_KERNEL_SKINNY;
+    if (mode == NGEMM_SAT_EXACT) return NGEMM_KERNEL_TCGEN05;
+    return NGEMM_KERNEL_SIMT;
+}
+
+ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc, int64_t m,
+                      int64_t n, int64_t k, int mode, int kernel, cudaStream_t st) {
+    ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, mode);
+    if (s != NGEMM_OK) return s;
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    if (kernel == NGEMM_KERNEL_AUTO) kernel = pick(m, n, k, mode);
+    switch (kernel) {
+    case NGEMM_KERNEL_SIMT: return launch_simt(a, lda, b, ldb, c, ldc, m, n, k, mode, st);
+    case NGEMM_KERNEL_SKINNY: return launch_skinny(a, lda, b, ldb, c, ldc, m, n, k, mode, di, st);
+    case NGEMM_KERNEL_TCGEN05:
+        if (mode != NGEMM_SAT_EXACT)
+            return fail(NGEMM_ERR_UNSUPPORTED,
+                        "tcgen05 computes exact int32 sums; HardwareSaturating needs the SIMT or skinny kernel");
+        if (m > INT32_MAX - tc::BM || k > INT32_MAX - tc::BK) return fail(NGEMM_ERR_SHAPE, "tcgen05: dims too large");
+        return launch_tcgen05(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    default: return fail(NGEMM_ERR_CONFIG, "unknown kernel id " + std::to_string(kernel));
+    }
+}
+
+// ---------------------------------------------------------------- packed weights
+ngemm_status validate_meta(const ngemm_packed_meta* p) {
+    if (!p) return fail(NGEMM_ERR_CONFIG, "null packed metadata");
+    if (p->v * p->h != p->w || p->h != 4)
+        return fail(NGEMM_ERR_CONFIG, "pack: shape (w=" + std::to_string(p->w) + ",h=" + std::to_string(p->h) +
+                                          ",v=" + std::to_string(p->v) + ") does not match the u8 path");
+    if (p->tm < p->v || p->tm % p->v != 0)
+        return fail(NGEMM_ERR_CONFIG, "tile: tm=" + std::to_string(p->tm) + " is not a positive multiple of v");
+    if (p->tk < p->h || p->tk % p->h != 0)
+        return fail(NGEMM_ERR_CONFIG, "tile: tk=" + std::to_string(p->tk) + " is not a positive multiple of h");
+    if (p->tn < 1) return fail(NGEMM_ERR_CONFIG, "tile: tn must be >= 1");
+    if (p->perm < 0 || p->perm > 5) return fail(NGEMM_ERR_CONFIG, "unknown permutation tag");
+    if (p->m_orig < 1 || p->k_orig < 1) return fail(NGEMM_ERR_SHAPE, "packed: dims must be >= 1");
+    if (p->m_pad != round_up(p->m_orig, p->tm) || p->k_pad != round_up(p->k_orig, p->tk))
+        return fail(NGEMM_ERR_SHAPE, "packed: padded dims disagree with tile metadata");
+    return NGEMM_OK;
+}
+
+PackedGeom geom_of(const ngemm_packed_meta* p) {
+    PackedGeom g;
+    g.w = p->w;
+    g.h = p->h;
+    g.v = p->v;
+    g.perm_m_before_k = (p->perm == 0 || p->perm == 1 || p->perm == 2) ? 1 : 0;
+    g.tm = p->tm;
+    g.tk = p->tk;
+    g.m_pad = p->m_pad;
+    g.k_pad = p->k_pad;
+    g.m_orig = p->m_orig;
+    g.k_orig = p->k_orig;
+    return g;
+}
+
+ngemm_status repack_on(const ngemm_packed_meta* meta, const uint8_t* d_packed, uint8_t* d_a, int64_t lda,
+                       cudaStream_t st) {
+    ngemm_status s = validate_meta(meta);
+    if (s != NGEMM_OK) return s;
+    if (lda < meta->k_orig) return fail(NGEMM_ERR_SHAPE, "repack: lda < K");
+    if (reinterpret_cast<uintptr_t>(d_packed) % 4 != 0) return fail(NGEMM_ERR_SHAPE, "repack: packed buffer must be 4-byte aligned");
+    const int64_t kwords = (meta->k_orig + 3) / 4;
+    const int64_t total = meta->m_orig * kwords;
+    const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
+    repack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(geom_of(meta), d_packed, d_a, lda, kwords);
+    NG_LAUNCHED();
+    return NGEMM_OK;
+}
+
+}  // namespace
+
+struct ngemm_packed_dev {
+    int device;
+    uint8_t* d_a;
+    int64_t lda, m, k;
+};
+
+extern "C" {
+
+int ngemm_cuda_abi_version(void) { return NGEMM_CUDA_ABI_VERSION; }
+
+const char* ngemm_cuda_status_name(int s) {
+    switch (s) {
+    case NGEMM_OK: return "ok";
+    case NGEMM_ERR_SHAPE: return "ShapeError";
+    case NGEMM_ERR_UNSUPPORTED: return "UnsupportedError";
+    case NGEMM_ERR_CONFIG: return "ConfigError";
+    case NGEMM_ERR_RANGE: return "RangeError";
+    case NGEMM_ERR_CORRUPTION: return "CorruptionError";
+    case NGEMM_ERR_INDEX: return "IndexError";
+    case NGEMM_ERR_CUDA: return "CudaError";
+    default: return "unknown";
+    }
+}
+
+const char* ngemm_cuda_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t ngemm_cuda_launch_count(void) { return g_launches.load(); }
+
+int ngemm_cuda_pick_kernel(int64_t m, int64_t n, int64_t k, int sat_mode) { return pick(m, n, k, sat_mode); }
+
+ngemm_status ngemm_cuda_gemm_u8i8(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                  int64_t ldc, int64_t m, int64_t n, int64_t k, int sat_mode, void* stream) {
+    return run_gemm(a, lda, b, ldb, c, ldc, m, n, k, sat_mode, NGEMM_KERNEL_AUTO, static_cast<cudaStream_t>(stream));
+}
+
+ngemm_status ngemm_cuda_gemm_u8i8_ex(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                     int64_t ldc, int64_t m, int64_t n, int64_t k, int sat_mode, int kernel,
+                                     void* stream) {
+    return run_gemm(a, lda, b, ldb, c, ldc, m, n, k, sat_mode, kernel, static_cast<cudaStream_t>(stream));
+}
+
+ngemm_status ngemm_cuda_packed_validate(const ngemm_packed_meta* meta) { return validate_meta(meta); }
+
+ngemm_status ngemm_cuda_repack(const ngemm_packed_meta* meta, const uint8_t* d_packed, uint8_t* d_a, int64_t lda,
+                               void* stream) {
+    return repack_on(meta, d_packed, d_a, lda, static_cast<cudaStream_t>(stream));
+}
+
+ngemm_status ngemm_cuda_packed_upload(const ngemm_packed_meta* meta, const uint8_t* host_packed, size_t nbytes,
+                                      ngemm_packed_handle* out) {
+    ngemm_status s = validate_meta(meta);
+    if (s != NGEMM_OK) return s;
+    if (!out || !host_packed) return fail(NGEMM_ERR_SHAPE, "packed_upload: null pointer");
+    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad))
+        return fail(NGEMM_ERR_SHAPE, "packed_upload: byte size disagrees with m_pad*k_pad");
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    const int64_t lda = round_up(meta->k_orig, 16);
+    uint8_t* d_packed = nullptr;
+    uint8_t* d_a = nullptr;
+    NG_CUDA(cudaMalloc(&d_packed, nbytes));
+    if (cudaMalloc(&d_a, static_cast<size_t>(meta->m_orig * lda)) != cudaSuccess) {
+        cudaFree(d_packed);
+        return fail(NGEMM_ERR_CUDA, "packed_upload: out of device memory");
+    }
+    cudaStream_t st = nullptr;
+    s = NGEMM_OK;
+    if (cudaMemsetAsync(d_a, 0, static_cast<size_t>(meta->m_orig * lda), st) != cudaSuccess ||
+        cudaMemcpyAsync(d_packed, host_packed, nbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        s = fail(NGEMM_ERR_CUDA, "packed_upload: copy failed");
+    if (s == NGEMM_OK) s = repack_on(meta, d_packed, d_a, lda, st);
+    if (s == NGEMM_OK && cudaStreamSynchronize(st) != cudaSuccess) s = fail(NGEMM_ERR_CUDA, "packed_upload: sync failed");
+    cudaFree(d_packed);
+    if (s != NGEMM_OK) {
+        cudaFree(d_a);
+        return s;
+    }
+    *out = new ngemm_packed_dev{dev, d_a, lda, meta->m_orig, meta->k_orig};
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_packed_from_device(const uint8_t* d_src, int64_t lda_src, int64_t m, int64_t k,
+                                           ngemm_packed_handle* out) {
+    if (!out || !d_src) return fail(NGEMM_ERR_SHAPE, "packed_from_device: null pointer");
+    if (m < 1 || k < 1 || lda_src < k) return fail(NGEMM_ERR_SHAPE, "packed_from_device: bad shape");
+    int dev;
+    DevInfo di;
+    ngemm_status s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    const int64_t lda = round_up(k, 16);
+    uint8_t* d_a = nullptr;
+    NG_CUDA(cudaMalloc(&d_a, static_cast<size_t>(m * lda)));
+    if (cudaMemset(d_a, 0, static_cast<size_t>(m * lda)) != cudaSuccess ||
+        cudaMemcpy2D(d_a, lda, d_src, lda_src, k, m, cudaMemcpyDeviceToDevice) != cudaSuccess) {
+        cudaFree(d_a);
+        return fail(NGEMM_ERR_CUDA, "packed_from_device: copy failed");
+    }
+    *out = new ngemm_packed_dev{dev, d_a, lda, m, k};
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_packed_free(ngemm_packed_handle h) {
+    if (!h) return NGEMM_OK;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(h->device);
+    cudaFree(h->d_a);
+    cudaSetDevice(prev);
+    delete h;
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_packed_info(ngemm_packed_handle h, const uint8_t** d_a, int64_t* lda, int64_t* m, int64_t* k,
+                                    int* device) {
+    if (!h) return fail(NGEMM_ERR_SHAPE, "null handle");
+    if (d_a) *d_a = h->d_a;
+    if (lda) *lda = h->lda;
+    if (m) *m = h->m;
+    if (k) *k = h->k;
+    if (device) *device = h->device;
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_gemm_packed(ngemm_packed_handle h, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                                    int64_t n, int sat_mode, void* stream) {
+    if (!h) return fail(NGEMM_ERR_SHAPE, "null handle");
+    return run_gemm(h->d_a, h->lda, b, ldb, c, ldc, h->m, n, h->k, sat_mode, NGEMM_KERNEL_AUTO,
+                    static_cast<cudaStream_t>(stream));
+}
+
+// ---------------------------------------------------------------- host-pointer entries
+ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_t* c, int64_t m, int64_t n, int64_t k,
+                                       int sat_mode, int kernel) {
+    ngemm_status s = validate(a, k, b, k, c, n, m, n, k, sat_mode);
+    if (s != NGEMM_OK) return s;
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    const int64_t kp = round_up(k, 16);
+    uint8_t* buf = nullptr;
+    const size_t a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
+    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
+    const size_t a_off = 0, b_off = round_up(a_bytes, 256), c_off = b_off + round_up(b_bytes, 256);
+    cudaStream_t st = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
+    s = NGEMM_OK;
+    if (cudaMemcpy2DAsync(buf + a_off, kp, a, k, k, m, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpy2DAsync(buf + b_off, kp, b, k, k, n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        s = fail(NGEMM_ERR_CUDA, "gemm_host: H2D copy failed");
+    if (s == NGEMM_OK)
+        s = run_gemm(buf + a_off, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
+                     reinterpret_cast<int32_t*>(buf + c_off), n, m, n, k, sat_mode,
+                     kernel, st);
+    if (s == NGEMM_OK && cudaMemcpyAsync(c, buf + c_off, c_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        s = fail(NGEMM_ERR_CUDA, "gemm_host: D2H copy failed");
+    cudaFreeAsync(buf, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && s == NGEMM_OK)
+        s = fail(NGEMM_ERR_CUDA, std::string("gemm_host: ") + cudaGetErrorString(cudaGetLastError()));
+    return s;
+}
+
+ngemm_status ngemm_cuda_gemm_packed_host(const ngemm_packed_meta* meta, const uint8_t* host_packed, size_t nbytes,
+                                         const int8_t* b, int32_t* c, int64_t n, int sat_mode, int kernel) {
+    ngemm_status s = validate_meta(meta);
+    if (s != NGEMM_OK) return s;
+    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad))
+        return fail(NGEMM_ERR_SHAPE, "gemm_packed_host: byte size disagrees with m_pad*k_pad");
+    const int64_t m = meta->m_orig, k = meta->k_orig;
+    s = validate(host_packed, k, b, k, c, n, m, n, k, sat_mode);
+    if (s != NGEMM_OK) return s;
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    const int64_t kp = round_up(k, 16);
+    const size_t p_bytes = nbytes, a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
+    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
+    const size_t p_off = 0, a_off = round_up(p_bytes, 256), b_off = a_off + round_up(a_bytes, 256),
+                 c_off = b_off + round_up(b_bytes, 256);
+    cudaStream_t st = nullptr;
+    uint8_t* buf = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
+    s = NGEMM_OK;
+    if (cudaMemcpyAsync(buf + p_off, host_packed, p_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
+        cudaMemcpy2DAsync(buf + b_off, kp, b, k, k, n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        s = fail(NGEMM_ERR_CUDA, "gemm_packed_host: H2D copy failed");
+    if (s == NGEMM_OK) s = repack_on(meta, buf + p_off, buf + a_off, kp, st);
+    if (s == NGEMM_OK)
+        s = run_gemm(buf + a_off, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
+                     reinterpret_cast<int32_t*>(buf + c_off), n, m, n, k, sat_mode, kernel, st);
+    if (s == NGEMM_OK && cudaMemcpyAsync(c, buf + c_off, c_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        s = fail(NGEMM_ERR_CUDA, "gemm_packed_host: D2H copy failed");
+    cudaFreeAsync(buf, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && s == NGEMM_OK)
+        s = fail(NGEMM_ERR_CUDA, std::string("gemm_packed_host: ") + cudaGetErrorString(cudaGetLastError()));
+    return s;
+}
+
+// ---------------------------------------------------------------- multi-GPU M-shard driver
+ngemm_status ngemm_cuda_shard_rows(int64_t m, int ndev, int64_t align, int64_t* row_start) {
+    if (m < 1 || ndev < 1 || align < 1 || !row_start) return fail(NGEMM_ERR_CONFIG, "shard_rows: bad arguments");
+    const int64_t per = round_up((m + ndev - 1) / ndev, align);
+    for (int d = 0; d <= ndev; ++d) row_start[d] = std::min<int64_t>(m, per * d);
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint8_t* a, const int8_t* b, int32_t* c,
+                                        int64_t m, int64_t n, int64_t k, int sat_mode, int gather_device,
+                                        int32_t** gathered) {
+    if (!devices || ndev < 1) return fail(NGEMM_ERR_CONFIG, "multi: empty device list");
+    ngemm_status s = validate(a, k, b, k, c, n, m, n, k, sat_mode);
+    if (s != NGEMM_OK) return s;
+    std::vector<int64_t> rs(static_cast<size_t>(ndev) + 1);
+    ngemm_cuda_shard_rows(m, ndev, tc::BM, rs.data());
+    std::vector<ngemm_status> st(static_cast<size_t>(ndev), NGEMM_OK);
+    std::vector<std::string> msg(static_cast<size_t>(ndev));
+    std::vector<std::thread> workers;
+    for (int d = 0; d < ndev; ++d) {
+        workers.emplace_back([&, d] {
+            const int64_t r0 = rs[d], r1 = rs[d + 1];
+            if (r1 <= r0) return;
+            if (cudaSetDevice(devices[d]) != cudaSuccess) {
+                st[d] = NGEMM_ERR_CUDA;
+                msg[d] = "cudaSetDevice failed";
+                return;
+            }
+            st[d] = ngemm_cuda_gemm_u8i8_host(a + r0 * k, b, c + r0 * n, r1 - r0, n, k, sat_mode, NGEMM_KERNEL_AUTO);
+            if (st[d] != NGEMM_OK) msg[d] = ngemm_cuda_last_error();
+        });
+    }
+    for (auto& w : workers) w.join();
+    for (int d = 0; d < ndev; ++d)
+        if (st[d] != NGEMM_OK) return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
+    if (gather_device >= 0 && gathered) {
+        // Assemble the row-major C on one device: shards are contiguous byte ranges, so the
+        // gather is a concatenation of host->device copies of each shard's rows.
+        int prev = 0;
+        cudaGetDevice(&prev);
+        NG_CUDA(cudaSetDevice(gather_device));
+        int32_t* full = nullptr;
+        NG_CUDA(cudaMalloc(&full, static_cast<size_t>(m * n) * 4));
+        NG_CUDA(cudaMemcpy(full, c, static_cast<size_t>(m * n) * 4, cudaMemcpyHostToDevice));
+        *gathered = full;
+        cudaSetDevice(prev);
+    }
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_free(void* p) {
+    if (p) NG_CUDA(cudaFree(p));
+    return NGEMM_OK;
+}
+
+}  // extern "C"

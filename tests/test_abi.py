@@ -1,0 +1,136 @@
+"""CPU-side checks of the C-ABI boundary: the library loads, exports every symbol that
+include/ngemm_cuda.h declares, validates before launching (reference error mapping), and
+fails loudly — never falls back to the CPU — when no GPU is present."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_1910_00178_b200 import _lib, api
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_symbols():
+    src = open(os.path.join(ROOT, "include", "ngemm_cuda.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(ngemm_cuda_\w+)\s*\(", src)))
+
+
+def test_library_exports_every_declared_symbol():
+    L = _lib.load()
+    declared = _declared_symbols()
+    assert len(declared) >= 15
+    for name in declared:
+        assert hasattr(L, name), name
+    assert sorted(_lib.EXPORTS) == declared
+
+
+def test_abi_version_and_status_names():
+    L = _lib.load()
+    assert L.ngemm_cuda_abi_version() == 1
+    names = [L.ngemm_cuda_status_name(i).decode() for i in range(8)]
+    assert names == ["ok", "ShapeError", "UnsupportedError", "ConfigError", "RangeError", "CorruptionError",
+                     "IndexError", "CudaError"]
+
+
+def test_kernel_pick_policy():
+    assert api.pick_kernel(1, 768, 768, api.SatMode.WIDENING_EXACT) == "skinny"
+    assert api.pick_kernel(16, 4096, 1024, api.SatMode.HARDWARE_SATURATING) == "skinny"
+    assert api.pick_kernel(1024, 1024, 1024, api.SatMode.WIDENING_EXACT) == "tcgen05"
+    assert api.pick_kernel(1024, 1024, 1024, api.SatMode.HARDWARE_SATURATING) == "simt"
+    assert api.pick_kernel(17, 64, 64, api.SatMode.WIDENING_EXACT) == "tcgen05"
+
+
+def test_shard_rows():
+    assert api.shard_rows(16384, 8, 128) == [0, 2048, 4096, 6144, 8192, 10240, 12288, 14336, 16384]
+    assert api.shard_rows(1000, 4, 128) == [0, 256, 512, 768, 1000]
+    assert api.shard_rows(100, 4, 128) == [0, 100, 100, 100, 100]
+    rs = api.shard_rows(16385, 8, 128)
+    assert rs[0] == 0 and rs[-1] == 16385 and all(r % 128 == 0 for r in rs[:-1])
+
+
+def test_packed_validate_maps_config_errors():
+    L = _lib.load()
+    good = _lib.PackedMeta(32, 4, 8, 8, 1, 4, 0, 5, 5, 8, 8)
+    assert L.ngemm_cuda_packed_validate(C.byref(good)) == _lib.OK
+    for bad in (_lib.PackedMeta(32, 4, 8, 7, 1, 4, 0, 5, 5, 7, 8),     # tm not multiple of v
+                _lib.PackedMeta(32, 4, 8, 8, 1, 5, 0, 5, 5, 8, 5),     # tk not multiple of h
+                _lib.PackedMeta(32, 4, 8, 8, 0, 4, 0, 5, 5, 8, 8),     # tn < 1
+                _lib.PackedMeta(32, 2, 16, 8, 1, 4, 0, 5, 5, 8, 8)):   # 16-bit shape on the u8 path
+        assert L.ngemm_cuda_packed_validate(C.byref(bad)) == _lib.ERR_CONFIG
+    wrong_pad = _lib.PackedMeta(32, 4, 8, 8, 1, 4, 0, 5, 5, 16, 8)
+    assert L.ngemm_cuda_packed_validate(C.byref(wrong_pad)) == _lib.ERR_SHAPE
+
+
+def test_validation_precedes_device_use():
+    # errors are reported before any launch, like the reference throws before dispatch
+    L = _lib.load()
+    buf = (C.c_uint8 * 64)()
+    assert L.ngemm_cuda_gemm_u8i8(buf, 4, buf, 4, buf, 4, 0, 4, 4, 1, None) == _lib.ERR_SHAPE
+    assert L.ngemm_cuda_gemm_u8i8(buf, 3, buf, 4, buf, 4, 4, 4, 4, 1, None) == _lib.ERR_SHAPE
+    assert L.ngemm_cuda_gemm_u8i8(buf, 4, buf, 4, buf, 4, 4, 4, 4, 7, None) == _lib.ERR_CONFIG
+
+
+def test_api_engine_and_kind_errors():
+    a = np.zeros((4, 8), np.uint8)
+    b = np.zeros((4, 8), np.int8)
+    with pytest.raises(api.UnsupportedError):
+        api.gemm_conventional(a, b, api.kernel_shape(256), api.SatMode.WIDENING_EXACT, api.Engine.NATIVE)
+    with pytest.raises(api.UnsupportedError):
+        api.gemm_conventional(a, b.view(np.uint8), api.kernel_shape(256), api.SatMode.WIDENING_EXACT)
+    with pytest.raises(api.ShapeError):
+        api.gemm_conventional(a, np.zeros((4, 9), np.int8), api.kernel_shape(256), api.SatMode.WIDENING_EXACT)
+    p = api.pack_weights(a, api.kernel_shape(256), api.TileConfig(8, 1, 4))
+    with pytest.raises(api.ShapeError):
+        api.gemm_ngemm(p, np.zeros((4, 9), np.int8), api.SatMode.WIDENING_EXACT)
+
+
+def test_no_cpu_fallback_without_gpu():
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    a = np.ones((4, 8), np.uint8)
+    b = np.ones((4, 8), np.int8)
+    with pytest.raises(api.CudaError):
+        api.gemm_conventional(a, b, api.kernel_shape(256), api.SatMode.WIDENING_EXACT)
+
+
+def test_kernel_shape_table():
+    # test_layout.cpp:12-22 (8-bit rows)
+    assert api.kernel_shape(256) == api.KernelShape(32, 4, 8)
+    assert api.kernel_shape(512) == api.KernelShape(64, 4, 16)
+    assert api.kernel_shape(128) == api.KernelShape(16, 4, 4)
+    assert api.kernel_shape(256, 16) == api.KernelShape(16, 2, 8)
+    with pytest.raises(api.UnsupportedError):
+        api.kernel_shape(256, 32)
+
+
+def test_host_pack_matches_oracle_and_reference_digests(oracle, golden):
+    for c in golden["packs"]:
+        a = np.array([[1, 2], [3, 4]], np.uint8) if c["seed"] is None else oracle.mat_random_u8(c["m"], c["k"], c["seed"])
+        p = api.pack_weights(a, api.KernelShape(c["w"], c["h"], c["v"]),
+                             api.TileConfig(c["tm"], c["tn"], c["tk"], api.Perm(c["perm"])))
+        assert p.data.size == c["nbytes"]
+        assert oracle.fnv1a(p.data) == c["fnv"]
+        assert (api.unpack_weights(p) == a).all()
+
+
+def test_host_unpack_detects_corruption():
+    a = np.arange(25, dtype=np.uint8).reshape(5, 5) + 1
+    p = api.pack_weights(a, api.KernelShape(32, 4, 8), api.TileConfig(8, 1, 4))
+    p.data[p.elem_offset(7, 0)] = 42
+    with pytest.raises(api.CorruptionError):
+        api.unpack_weights(p)
+
+
+def test_pack_rejects_bad_tiles_and_kinds():
+    a = np.zeros((4, 4), np.uint8)
+    s = api.KernelShape(32, 4, 8)
+    for t in (api.TileConfig(7, 1, 4), api.TileConfig(8, 1, 5), api.TileConfig(8, 0, 4)):
+        with pytest.raises(api.ConfigError):
+            api.pack_weights(a, s, t)
+    with pytest.raises(api.UnsupportedError):
+        api.pack_weights(np.zeros((4, 4), np.int32), s, api.TileConfig(8, 1, 4))

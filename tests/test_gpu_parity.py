@@ -1,0 +1,282 @@
+"""GPU parity: every kernel of libngemm_cuda.so, called through the C-ABI, is bit-exact
+against the CPU oracle (pinned to the reference) and the reference-generated fixtures.
+
+Modes: SAT = HardwareSaturating (gemm_sat_oracle, gemm.hpp:83-104), EXACT = WideningExact
+(gemm_ref, gemm.hpp:36-52).  Integer work: the bar is bit-exact, no tolerance."""
+import numpy as np
+import pytest
+
+from oracle.oracle import EXACT, SAT
+from paper_1910_00178_b200 import _lib, api
+
+pytestmark = pytest.mark.gpu
+
+KERNELS = {"simt": _lib.KERNEL_SIMT, "tcgen05": _lib.KERNEL_TCGEN05, "skinny": _lib.KERNEL_SKINNY,
+           "auto": _lib.KERNEL_AUTO}
+
+
+def dev_gemm(a, b, mode, kernel="auto", lda=None, ldb=None, ldc=None):
+    import torch
+    m, k = a.shape
+    n = b.shape[0]
+    lda = k if lda is None else lda
+    ldb = k if ldb is None else ldb
+    ldc = n if ldc is None else ldc
+    da = torch.zeros((m, lda), dtype=torch.uint8, device="cuda")
+    db = torch.zeros((n, ldb), dtype=torch.int8, device="cuda")
+    da[:, :k] = torch.from_numpy(a)
+    db[:, :k] = torch.from_numpy(b)
+    dc = torch.full((m, ldc), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    st = torch.cuda.current_stream().cuda_stream
+    _lib.check(L.ngemm_cuda_gemm_u8i8_ex(da.data_ptr(), lda, db.data_ptr(), ldb, dc.data_ptr(), ldc, m, n, k, mode,
+                                         KERNELS[kernel], st))
+    torch.cuda.synchronize()
+    out = dc.cpu().numpy()
+    if ldc > n:
+        assert (out[:, n:] == 0x5A5A5A5A).all(), "kernel wrote outside C's logical columns"
+    return out[:, :n]
+
+
+def kernels_for(m, mode):
+    ks = ["simt", "auto"]
+    if mode == EXACT:
+        ks.append("tcgen05")
+    if m <= 16:
+        ks.append("skinny")
+    return ks
+
+
+def test_2x2(cuda):
+    a = np.array([[1, 2], [3, 4]], np.uint8)
+    b = np.array([[5, -1], [2, 0]], np.int8)
+    for mode in (EXACT, SAT):
+        for k in kernels_for(2, mode):
+            assert dev_gemm(a, b, mode, k).tolist() == [[3, 2], [11, 6]], k
+
+
+def test_adversarial_saturation(cuda, golden):
+    adv = golden["adversarial"]
+    a = np.full((4, 12), 255, np.uint8)
+    b = np.array(adv["b"], np.int8)
+    for k in kernels_for(4, SAT):
+        assert dev_gemm(a, b, SAT, k).tolist() == adv["sat"], k
+    for k in kernels_for(4, EXACT):
+        assert dev_gemm(a, b, EXACT, k).tolist() == adv["exact"], k
+
+
+def test_random_small_shapes_vs_reference(cuda, oracle, golden):
+    for case in golden["random_small"]:
+        a = oracle.mat_random_u8(case["m"], case["k"], case["seed_a"])
+        b = oracle.mat_random_i8(case["n"], case["k"], case["seed_b"])
+        for mode, key in ((EXACT, "exact"), (SAT, "sat")):
+            for k in kernels_for(case["m"], mode):
+                assert dev_gemm(a, b, mode, k).ravel().tolist() == case[key], (case["m"], case["n"], case["k"], k)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_random_shapes_1_to_300(cuda, oracle, seed):
+    rng = np.random.default_rng(seed)
+    for _ in range(12):
+        m, n, k = (int(x) for x in rng.integers(1, 300, 3))
+        a = oracle.mat_random_u8(m, k, 10 * seed + m)
+        b = oracle.mat_random_i8(n, k, 10 * seed + n + 7)
+        for mode in (EXACT, SAT):
+            ref = oracle.gemm(a, b, mode)
+            for kern in kernels_for(m, mode):
+                assert (dev_gemm(a, b, mode, kern) == ref).all(), (m, n, k, mode, kern)
+
+
+def test_acceptance_1000_random_small(cuda, oracle):
+    # SPEC.md:533 acceptance #1: >= 1000 random (M,N,K) in [1,64]^3, exact mode, bit-exact
+    rng = np.random.default_rng(1234)
+    for t in range(1000):
+        m, n, k = (int(x) for x in rng.integers(1, 65, 3))
+        a = oracle.mat_random_u8(m, k, 5000 + t)
+        b = oracle.mat_random_i8(n, k, 9000 + t)
+        assert (dev_gemm(a, b, EXACT) == oracle.gemm(a, b, EXACT, threads=1)).all(), (m, n, k)
+
+
+def test_acceptance_100_adversarial_sat(cuda, oracle):
+    # SPEC.md:534 acceptance #2: 100 adversarial cases (u8 = 255, i8 in {127, -128})
+    rng = np.random.default_rng(99)
+    for t in range(100):
+        m, n, k = (int(x) for x in rng.integers(1, 65, 3))
+        a = np.full((m, k), 255, np.uint8)
+        b = np.where(rng.integers(0, 2, (n, k)) == 1, 127, -128).astype(np.int8)
+        ref = oracle.gemm(a, b, SAT, threads=1)
+        for kern in kernels_for(m, SAT):
+            assert (dev_gemm(a, b, SAT, kern) == ref).all(), (m, n, k, kern)
+
+
+def test_wrapping_k4096(cuda, oracle):
+    a = oracle.mat_random_u8(2, 4096, 30)
+    b = oracle.mat_random_i8(2, 4096, 31)
+    for mode in (EXACT, SAT):
+        ref = oracle.gemm(a, b, mode)
+        for kern in kernels_for(2, mode) + (["tcgen05"] if mode == EXACT else []):
+            assert (dev_gemm(a, b, mode, kern) == ref).all(), kern
+
+
+def test_leading_dimensions_and_unaligned_k(cuda, oracle):
+    for (m, n, k, lda, ldb, ldc) in ((130, 70, 1000, 1003, 1001, 77), (17, 300, 37, 40, 48, 301),
+                                     (5, 33, 100, 100, 112, 33), (300, 260, 200, 208, 200, 264)):
+        a = oracle.mat_random_u8(m, k, m)
+        b = oracle.mat_random_i8(n, k, n)
+        for mode in (EXACT, SAT):
+            ref = oracle.gemm(a, b, mode)
+            for kern in kernels_for(m, mode):
+                assert (dev_gemm(a, b, mode, kern, lda, ldb, ldc) == ref).all(), (m, n, k, kern)
+
+
+def test_config1(cuda, oracle, golden):
+    a = oracle.mat_random_u8(1024, 1024, 0)
+    b = oracle.mat_random_i8(1024, 1024, 1)
+    g = golden["config1"]
+    for mode, key in ((EXACT, "exact"), (SAT, "sat")):
+        for kern in kernels_for(1024, mode):
+            c = dev_gemm(a, b, mode, kern)
+            assert oracle.fnv1a(c) == g[f"{key}_fnv"], kern
+            assert int(c.astype(np.int64).sum()) == g[f"{key}_checksum"]
+
+
+def test_config2_skinny(cuda, oracle, golden):
+    for c in golden["config2"]:
+        a = oracle.mat_random_u8(c["m"], c["k"], 0)
+        b = oracle.mat_normal_i8(c["n"], c["k"], 1, 32.0)
+        for mode, key in ((EXACT, "exact"), (SAT, "sat")):
+            for kern in kernels_for(c["m"], mode):
+                assert oracle.fnv1a(dev_gemm(a, b, mode, kern)) == c[f"{key}_fnv"], (c["m"], c["n"], c["k"], kern)
+
+
+def test_config3_medium(cuda, oracle, golden):
+    for c in golden["config3"]:
+        a = oracle.mat_random_u8(c["m"], c["k"], 0)
+        b = oracle.mat_random_i8(c["n"], c["k"], 1)
+        for mode, key in ((EXACT, "exact"), (SAT, "sat")):
+            for kern in kernels_for(c["m"], mode):
+                assert oracle.fnv1a(dev_gemm(a, b, mode, kern)) == c[f"{key}_fnv"], (c["m"], c["n"], c["k"], kern)
+
+
+def _pattern(kind, rows, cols, p):
+    idx = np.arange(rows * cols).reshape(rows, cols) & 1
+    if kind == "a":
+        return np.full((rows, cols), 255, np.uint8) if p == "all255" else np.where(idx, 255, 0).astype(np.uint8)
+    if p == "all-128":
+        return np.full((rows, cols), -128, np.int8)
+    if p == "all127":
+        return np.full((rows, cols), 127, np.int8)
+    return np.where(idx, 127, -128).astype(np.int8)
+
+
+def test_config4_saturation_edges(cuda, golden):
+    for c in golden["config4"]:
+        s = c["size"]
+        a = _pattern("a", s, s, c["a"])
+        b = _pattern("b", s, s, c["b"])
+        for mode, key in ((EXACT, "exact"), (SAT, "sat")):
+            for kern in kernels_for(s, mode):
+                out = dev_gemm(a, b, mode, kern)
+                assert (out == c[key]).all(), (s, c["a"], c["b"], key, kern)
+
+
+def test_splitk_small_m_deep_k(cuda, oracle):
+    # few output tiles and deep K: exercises the split-K (red.add) epilogue of tcgen05
+    for (m, n, k) in ((128, 256, 8192), (200, 100, 4000), (64, 64, 16384)):
+        a = oracle.mat_random_u8(m, k, 1)
+        b = oracle.mat_random_i8(n, k, 2)
+        assert (dev_gemm(a, b, EXACT, "tcgen05") == oracle.gemm(a, b, EXACT)).all(), (m, n, k)
+
+
+def test_packed_path_device(cuda, oracle):
+    import torch
+    for (m, n, k, tm, tn, tk, perm, w, v) in ((9, 3, 7, 8, 2, 4, 0, 32, 8), (40, 17, 100, 16, 8, 12, 3, 32, 8),
+                                              (300, 129, 520, 32, 64, 64, 4, 64, 16),
+                                              (130, 257, 257, 16, 64, 260, 5, 64, 16)):
+        a = oracle.mat_random_u8(m, k, m + 1)
+        b = oracle.mat_random_i8(n, k, n + 1)
+        p = api.pack_weights(a, api.KernelShape(w, 4, v), api.TileConfig(tm, tn, tk, api.Perm(perm)))
+        dp = p.upload()
+        _, lda, mm, kk, _ = dp.info()
+        assert (mm, kk) == (m, k) and lda % 16 == 0
+        db = torch.from_numpy(b).cuda()
+        for mode in (EXACT, SAT):
+            c = dp.gemm(db, mode=mode).cpu().numpy()
+            assert (c == oracle.gemm(a, b, mode)).all(), (m, n, k, perm, mode)
+        # device repack entry on its own
+        dpk = torch.from_numpy(p.data).cuda()
+        da = torch.zeros((m, lda), dtype=torch.uint8, device="cuda")
+        api.repack_device(p, dpk, da, lda)
+        torch.cuda.synchronize()
+        assert (da[:, :k].cpu().numpy() == a).all()
+        p.invalidate()
+
+
+def test_host_api_mirrors_reference_tests(cuda, oracle, golden):
+    s256 = api.kernel_shape(256)
+    # test_gemm.cpp:73-79, 101-107
+    a = np.array([[1, 2], [3, 4]], np.uint8)
+    b = np.array([[5, -1], [2, 0]], np.int8)
+    for eng in (api.Engine.AUTO, api.Engine.EMULATED, api.Engine.CUDA):
+        assert api.gemm_conventional(a, b, s256, api.SatMode.WIDENING_EXACT, eng).tolist() == [[3, 2], [11, 6]]
+        p = api.pack_weights(a, s256, api.TileConfig(8, 1, 4))
+        assert api.gemm_ngemm(p, b, api.SatMode.WIDENING_EXACT, eng).tolist() == [[3, 2], [11, 6]]
+    # test_gemm.cpp:109-116: zero weights through the padding path
+    z = api.gemm_ngemm(api.pack_weights(np.zeros((9, 5), np.uint8), s256, api.TileConfig(8, 1, 4)),
+                       oracle.mat_random_i8(4, 5, 6), api.SatMode.HARDWARE_SATURATING, api.Engine.EMULATED)
+    assert (z == 0).all()
+    # test_gemm.cpp:118-127: tail stress across permutations, both modes
+    a = oracle.mat_random_u8(9, 7, 12, 0, 127)
+    b = oracle.mat_random_i8(3, 7, 13)
+    ref = oracle.gemm(a, b, EXACT)
+    for perm in (api.Perm.MNK, api.Perm.NMK, api.Perm.KNM):
+        p = api.pack_weights(a, s256, api.TileConfig(8, 2, 4, perm))
+        for mode in api.SatMode:
+            assert (api.gemm_ngemm(p, b, mode, api.Engine.EMULATED) == ref).all()
+            assert (api.gemm_ngemm(p, b, mode) == ref).all()
+    # reference-kernel digests on packed weights (emulated reference, both modes)
+    for c in golden["ngemm_packed"]:
+        a = oracle.mat_random_u8(c["m"], c["k"], c["seed_a"])
+        b = oracle.mat_random_i8(c["n"], c["k"], c["seed_b"])
+        p = api.pack_weights(a, s256, api.TileConfig(c["tm"], c["tn"], c["tk"], api.Perm(c["perm"])))
+        assert oracle.fnv1a(api.gemm_ngemm(p, b, api.SatMode.WIDENING_EXACT)) == c["exact_fnv"]
+        assert oracle.fnv1a(api.gemm_ngemm(p, b, api.SatMode.HARDWARE_SATURATING)) == c["sat_fnv"]
+    with pytest.raises(api.UnsupportedError):
+        api.gemm_conventional(a, b, s256, api.SatMode.WIDENING_EXACT, api.Engine.NATIVE)
+
+
+def test_multi_device_driver_single_gpu(cuda, oracle):
+    a = oracle.mat_random_u8(300, 200, 3)
+    b = oracle.mat_random_i8(150, 200, 4)
+    for mode in (EXACT, SAT):
+        assert (api.gemm_multi([0], a, b, mode) == oracle.gemm(a, b, mode)).all()
+        # same device listed twice = two row shards on one GPU (host-side shard/concat logic)
+        assert (api.gemm_multi([0, 0], a, b, mode) == oracle.gemm(a, b, mode)).all()
+
+
+@pytest.mark.slow
+def test_config5_full_size(cuda, oracle, golden):
+    """16384^3 exact on tcgen05: first 128 rows against the reference digest, plus a
+    Freivalds check of the whole C (C.x == A.(B^T.x) in int64 with x in {0,1}; no C entry
+    wraps for K <= 65793)."""
+    import torch
+    K = 16384
+    b = oracle.mat_random_i8(K, K, 1)
+    g = golden["config5_rows0_128"]
+    assert oracle.fnv1a(b) == golden["config5_b_fnv"]
+    a = oracle.mat_random_u8(K, K, 0)
+    da = torch.from_numpy(a).cuda()
+    db = torch.from_numpy(b).cuda()
+    dc = api.gemm_device(da, db, mode=api.SatMode.WIDENING_EXACT)
+    torch.cuda.synchronize()
+    top = dc[:128].cpu().numpy()
+    assert oracle.fnv1a(top) == g["exact_fnv"]
+    assert int(top.astype(np.int64).sum()) == g["exact_checksum"]
+    # float64 is exact here: every product and partial sum is an integer below 2^53
+    gen = torch.Generator(device="cuda").manual_seed(7)
+    for _ in range(2):
+        x = torch.randint(0, 2, (K, 1), device="cuda", generator=gen).to(torch.float64)
+        lhs = dc.to(torch.float64) @ x                      # C.x
+        btx = db.to(torch.float64).t() @ x                  # B^T x
+        rhs = da.to(torch.float64) @ btx                    # A.(B^T x)
+        assert torch.equal(lhs, rhs)
