@@ -74,8 +74,23 @@ DevInfo dev_info(int dev) {
     return d;
 }
 
+// Keep freed stream-ordered allocations cached in the device pool (the default release
+// threshold of 0 would return them to the OS at every synchronisation, turning each
+// host-entry call into a fresh multi-GB mapping).
+void keep_pool(int dev) {
+    static std::once_flag once[64];
+    std::call_once(once[dev & 63], [dev] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+            uint64_t thr = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+        }
+    });
+}
+
 ngemm_status current_device(int* dev, DevInfo* info) {
     NG_CUDA(cudaGetDevice(dev));
+    keep_pool(*dev);
     *info = dev_info(*dev);
     if (info->sms <= 0) return fail(NGEMM_ERR_CUDA, "no CUDA device");
     if (info->cc_major != 10 || info->cc_minor != 0)
@@ -269,6 +284,12 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
                       : launch_tc_t<256, 4>(ta, tb, c, ldc, m, n, k, di, st);
     if (scratch) cudaFreeAsync(scratch, st);
     return s;
+}
+
+// Host rows of `k` bytes -> device rows of pitch `kp` (one 1-D copy when the pitches agree).
+cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int64_t rows, cudaStream_t st) {
+    if (kp == k) return cudaMemcpyAsync(dst, src, static_cast<size_t>(rows * k), cudaMemcpyHostToDevice, st);
+    return cudaMemcpy2DAsync(dst, kp, src, k, k, rows, cudaMemcpyHostToDevice, st);
 }
 
 int pick(int64_t m, int64_t n, int64_t k, int mode) {
@@ -498,8 +519,8 @@ ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_
     cudaStream_t st = nullptr;
     NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
     s = NGEMM_OK;
-    if (cudaMemcpy2DAsync(buf + a_off, kp, a, k, k, m, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpy2DAsync(buf + b_off, kp, b, k, k, n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+    if (copy_rows_h2d(buf + a_off, kp, a, k, m, st) != cudaSuccess ||
+        copy_rows_h2d(buf + b_off, kp, b, k, n, st) != cudaSuccess)
         s = fail(NGEMM_ERR_CUDA, "gemm_host: H2D copy failed");
     if (s == NGEMM_OK)
         s = run_gemm(buf + a_off, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
@@ -536,7 +557,7 @@ ngemm_status ngemm_cuda_gemm_packed_host(const ngemm_packed_meta* meta, const ui
     NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
     s = NGEMM_OK;
     if (cudaMemcpyAsync(buf + p_off, host_packed, p_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        cudaMemcpy2DAsync(buf + b_off, kp, b, k, k, n, cudaMemcpyHostToDevice, st) != cudaSuccess)
+        copy_rows_h2d(buf + b_off, kp, b, k, n, st) != cudaSuccess)
         s = fail(NGEMM_ERR_CUDA, "gemm_packed_host: H2D copy failed");
     if (s == NGEMM_OK) s = repack_on(meta, buf + p_off, buf + a_off, kp, st);
     if (s == NGEMM_OK)
