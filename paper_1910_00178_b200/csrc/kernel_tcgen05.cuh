@@ -7,15 +7,18 @@
 // tcgen05.mma kind::i8 with A unsigned, B signed and saturate = 0 accumulates in int32
 // modulo 2^32 exactly like gemm_ref / wrap_add_i32 (gemm.hpp:46-50, common.hpp:132-135).
 //
-// Structure (persistent, warp-specialised, one CTA per SM):
-//   warp 0      : TMA producer — A and B tiles (128-byte K slabs, SWIZZLE_128B) into a
-//                 STAGES-deep shared-memory ring guarded by full/empty mbarriers;
-//   warp 1      : MMA issuer — one elected thread issues BK/32 tcgen05.mma per stage into a
-//                 TMEM accumulator (double-buffered across tiles), tcgen05.commit frees stages;
-//   warp 2      : TMEM allocator;
-//   warps 4..7  : epilogue — tcgen05.ld (32 lanes x 32 columns per warp per step) -> registers
-//                 -> 128-byte row segments of C, overlapped with the next tile's MMAs.
-// Split-K (kSplit > 1) writes through red.global.add on a zeroed C; integer wrap-add is
+// Structure (persistent, warp-specialised, one CTA per SM; CG = 2 pairs the two SMs of a
+// TPC into one cluster that computes a 256 x BN tile with cta_group::2 MMAs):
+//   warp 0      : TMA producer — this CTA's 128 rows of A and BN/CG rows of B per 128-byte
+//                 K slab (SWIZZLE_128B) into a STAGES-deep smem ring (full/empty mbarriers;
+//                 with CG = 2 both CTAs' loads complete on the leader's full barrier);
+//   warp 1      : MMA issuer (leader CTA only) — one thread issues BK/32 tcgen05.mma per
+//                 stage into a double-buffered TMEM accumulator; tcgen05.commit (multicast
+//                 to the pair) frees the stage in both CTAs and publishes finished tiles;
+//   warp 2      : TMEM allocator (cta_group::CG);
+//   warps 4..7  : epilogue — tcgen05.ld 32 lanes x 32 columns -> registers -> 128-byte row
+//                 segments of C, overlapped with the next tile's MMAs.
+// Split-K (splits > 1) writes through atomic adds on a zeroed C; integer wrap-add is
 // associative, so split-K is bit-exact.
 #pragma once
 
@@ -24,16 +27,16 @@
 namespace ngemm_dev {
 
 namespace tc {
-constexpr int BM = 128;       // UMMA M per CTA
+constexpr int BM = 128;       // rows of A per CTA (UMMA M = 128 * CG)
 constexpr int BK = 128;       // bytes of K per stage (one SWIZZLE_128B row)
 constexpr int UMMA_K = 32;    // K per tcgen05.mma kind::i8
 constexpr int THREADS = 256;  // 8 warps
-constexpr int GROUP_M = 16;   // rasterisation group (L2 reuse of B across consecutive tiles)
+constexpr int GROUP_M = 8;    // rasterisation group (measured best of 4..64 at 16384^3, profiles/groupm)
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 struct Smem {
     static constexpr int A_BYTES = BM * BK;
-    static constexpr int B_BYTES = BN * BK;
+    static constexpr int B_BYTES = (BN / CG) * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
@@ -44,27 +47,29 @@ struct Smem {
 }  // namespace tc
 
 struct TileMap {
-    int tiles_m, tiles_n, splits;
+    int tiles_m, tiles_n, splits;  // tiles_m counts 128*CG-row tiles
+    int group_m;                   // rasterisation: group_m M-tiles walked down before moving along N
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
         t -= ks * per_split;
-        const int group_size = tc::GROUP_M * tiles_n;
+        const int group_size = group_m * tiles_n;
         const int g = t / group_size;
-        const int first_m = g * tc::GROUP_M;
-        const int gm = min(tiles_m - first_m, tc::GROUP_M);
+        const int first_m = g * group_m;
+        const int gm = min(tiles_m - first_m, group_m);
         const int r = t - g * group_size;
         tm = first_m + r % gm;
         tn = r / gm;
     }
 };
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    int32_t* __restrict__ C, int64_t ldc, int M, int N, int num_kb_total, TileMap map,
                    int c_vec_ok) {
-    using S = tc::Smem<BN, STAGES>;
+    using S = tc::Smem<BN, STAGES, CG>;
+    constexpr int UMMA_M = tc::BM * CG;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFFSET);
@@ -74,6 +79,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;  // 0 = pair leader
+    const int unit = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+    const int num_units = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
     const int num_tiles = map.tiles_m * map.tiles_n * map.splits;
     const int kb_per_split = (num_kb_total + map.splits - 1) / map.splits;
 
@@ -86,48 +94,56 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
-            mbar_init(&tempty[s], 128);
+            mbar_init(&tempty[s], 4 * CG);  // one arrival per epilogue warp of every CTA
         }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<1>(tmem_slot, S::TMEM_COLS);
+    if (warp == 2) tmem_alloc<CG>(tmem_slot, S::TMEM_COLS);
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0) {
         if (lane == 0) {
-            // ---------------- TMA producer
-            const uint64_t pol_a = policy_evict_normal();
-            const uint64_t pol_b = policy_evict_normal();
+            // ---------------- TMA producer (both CTAs)
+            const uint64_t pol = policy_evict_normal();
             int s = 0;
             uint32_t ph = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int t = unit; t < num_tiles; t += num_units) {
                 int tm, tn, ks;
                 map.coords(t, tm, tn, ks);
                 const int kb0 = ks * kb_per_split;
                 const int kb1 = min(num_kb_total, kb0 + kb_per_split);
+                const int row_a = tm * UMMA_M + static_cast<int>(rank) * tc::BM;
+                const int row_b = tn * BN + static_cast<int>(rank) * (BN / CG);
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&empty[s], ph ^ 1);
-                    mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
                     uint8_t* sa = smem + s * S::A_BYTES;
                     uint8_t* sb = smem + STAGES * S::A_BYTES + s * S::B_BYTES;
-                    tma_load_2d(sa, &tma_a, &full[s], kb * tc::BK, tm * tc::BM, pol_a);
-                    tma_load_2d(sb, &tma_b, &full[s], kb * tc::BK, tn * BN, pol_b);
+                    if constexpr (CG == 1) {
+                        mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
+                        tma_load_2d(sa, &tma_a, &full[s], kb * tc::BK, row_a, pol);
+                        tma_load_2d(sb, &tma_b, &full[s], kb * tc::BK, row_b, pol);
+                    } else {
+                        // both CTAs' bytes land on the leader's full barrier; the leader arms it
+                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
+                        tma_load_2d_cg2(sa, &tma_a, &full[s], kb * tc::BK, row_a, pol);
+                        tma_load_2d_cg2(sb, &tma_b, &full[s], kb * tc::BK, row_b, pol);
+                    }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {
-            // ---------------- MMA issuer (single thread)
-            constexpr uint32_t idesc = idesc_i8(tc::BM, BN, /*a_signed=*/false, /*b_signed=*/true);
+        if (lane == 0 && rank == 0) {
+            // ---------------- MMA issuer (single thread of the leader CTA)
+            constexpr uint32_t idesc = idesc_i8(UMMA_M, BN, /*a_signed=*/false, /*b_signed=*/true);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
-            for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+            for (int t = unit; t < num_tiles; t += num_units) {
                 int tm, tn, ks;
                 map.coords(t, tm, tn, ks);
                 const int kb0 = ks * kb_per_split;
@@ -142,30 +158,32 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     const uint32_t sb = smem_u32(smem + STAGES * S::A_BYTES + s * S::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < tc::BK / tc::UMMA_K; ++k) {
-                        mma_i8<1>(d_tmem, sdesc_k_sw128(sa + k * tc::UMMA_K), sdesc_k_sw128(sb + k * tc::UMMA_K),
-                                  idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                        mma_i8<CG>(d_tmem, sdesc_k_sw128(sa + k * tc::UMMA_K), sdesc_k_sw128(sb + k * tc::UMMA_K),
+                                   idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     }
-                    mma_commit(&empty[s]);
+                    if constexpr (CG == 1) mma_commit(&empty[s]);
+                    else mma_commit_cg2_mc(&empty[s], 0x3);
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
-                mma_commit(&tfull[acc]);
+                if constexpr (CG == 1) mma_commit(&tfull[acc]);
+                else mma_commit_cg2_mc(&tfull[acc], 0x3);
                 acc ^= 1;
                 if (acc == 0) acc_ph ^= 1;
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue: TMEM -> registers -> global
+        // ---------------- epilogue (both CTAs): TMEM -> registers -> global
         const int ew = warp & 3;  // TMEM lane quadrant this warp may access
         int acc = 0;
         uint32_t acc_ph = 0;
-        for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        for (int t = unit; t < num_tiles; t += num_units) {
             int tm, tn, ks;
             map.coords(t, tm, tn, ks);
             const int kb0 = ks * kb_per_split;
             const bool has_k = kb0 < num_kb_total;
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
-            const int64_t row = static_cast<int64_t>(tm) * tc::BM + ew * 32 + lane;
+            const int64_t row = static_cast<int64_t>(tm) * UMMA_M + rank * tc::BM + ew * 32 + lane;
             const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
             int32_t* crow = C + row * ldc;
 #pragma unroll 1
@@ -193,17 +211,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&tempty[acc]);
+            __syncwarp();
+            if (lane == 0) {
+                if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
+                else mbar_arrive_cluster(&tempty[acc], 0);
+            }
             acc ^= 1;
             if (acc == 0) acc_ph ^= 1;
         }
     }
 
     tc_fence_before();
-    __syncthreads();
+    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<1>(tmem_base, S::TMEM_COLS);
+        tmem_dealloc<CG>(tmem_base, S::TMEM_COLS);
     }
 }
 

@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <atomic>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -220,32 +221,49 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
                                    : launch_skinny_mode<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int CG>
 ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, int32_t* c, int64_t ldc, int64_t m,
-                         int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
-    using S = tc::Smem<BN, STAGES>;
+                         int64_t n, int64_t k, int splits_hint, const DevInfo& di, cudaStream_t st) {
+    using S = tc::Smem<BN, STAGES, CG>;
+    auto kern = tc_gemm_kernel<BN, STAGES, CG>;
     static std::once_flag once[64];
     int dev = 0;
     cudaGetDevice(&dev);
     ngemm_status s = NGEMM_OK;
-    std::call_once(once[dev & 63], [&] { s = set_smem(tc_gemm_kernel<BN, STAGES>, S::TOTAL); });
+    std::call_once(once[dev & 63], [&] { s = set_smem(kern, S::TOTAL); });
     if (s != NGEMM_OK) return s;
     TileMap map;
-    map.tiles_m = static_cast<int>((m + tc::BM - 1) / tc::BM);
+    map.tiles_m = static_cast<int>((m + tc::BM * CG - 1) / (tc::BM * CG));
     map.tiles_n = static_cast<int>((n + BN - 1) / BN);
     const int num_kb = static_cast<int>((k + tc::BK - 1) / tc::BK);
     const int tiles = map.tiles_m * map.tiles_n;
+    const int units = di.sms / CG;
     int splits = 1;
-    if (tiles * 2 <= di.sms && num_kb >= 8) splits = std::max(1, std::min(num_kb / 4, di.sms / tiles));
+    if (splits_hint > 0) splits = std::min(splits_hint, num_kb);
+    else if (tiles * 2 <= units && num_kb >= 8) splits = std::max(1, std::min(num_kb / 4, units / tiles));
     map.splits = splits;
+    map.group_m = tc::GROUP_M;
+    if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
     if (splits > 1) {
         if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
         else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
     }
     const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
-    const int grid = std::min(tiles * splits, di.sms);
-    tc_gemm_kernel<BN, STAGES><<<grid, tc::THREADS, S::TOTAL, st>>>(ta, tb, c, ldc, static_cast<int>(m),
-                                                                   static_cast<int>(n), num_kb, map, c_vec);
+    const int grid = std::min(tiles * splits, units) * CG;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::THREADS);
+    cfg.dynamicSmemBytes = S::TOTAL;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CG;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    NG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, c, ldc, static_cast<int>(m), static_cast<int>(n), num_kb, map,
+                               c_vec));
     NG_LAUNCHED();
     return NGEMM_OK;
 }
@@ -275,13 +293,20 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
             ldb_use = kp;
         }
     }
-    const int bn = (n <= 128) ? 128 : 256;
+    // Tile choice: 256 x 256 cta_group::2 pairs when there is enough work to fill the 74 SM
+    // pairs; otherwise single-CTA 128 x BN tiles (more tiles, plus split-K, for small shapes).
+    const int64_t tiles_pair = ((m + 255) / 256) * ((n + 255) / 256);
+    int cfg = (tiles_pair >= di.sms / 2) ? 2 : (n <= 128 ? 0 : 1);
+    if (const char* force = std::getenv("NGEMM_TC_CFG")) cfg = std::atoi(force) % 3;  // experiments only
+    const int bn_load = cfg == 2 ? 128 : (cfg == 0 ? 128 : 256);
     CUtensorMap ta, tb;
     ngemm_status s = make_tmap_u8(&ta, a_use, k, m, lda_use, tc::BK, tc::BM);
-    if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, bn);
-    if (s == NGEMM_OK)
-        s = bn == 128 ? launch_tc_t<128, 6>(ta, tb, c, ldc, m, n, k, di, st)
-                      : launch_tc_t<256, 4>(ta, tb, c, ldc, m, n, k, di, st);
+    if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, bn_load);
+    if (s == NGEMM_OK) {
+        if (cfg == 2) s = launch_tc_t<256, 6, 2>(ta, tb, c, ldc, m, n, k, 0, di, st);
+        else if (cfg == 0) s = launch_tc_t<128, 6, 1>(ta, tb, c, ldc, m, n, k, 0, di, st);
+        else s = launch_tc_t<256, 4, 1>(ta, tb, c, ldc, m, n, k, 0, di, st);
+    }
     if (scratch) cudaFreeAsync(scratch, st);
     return s;
 }
