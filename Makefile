@@ -12,7 +12,7 @@ all: $(LIB) oracle
 
 $(LIB): $(wildcard $(CSRC)/*.cu $(CSRC)/*.cuh) include/ngemm_cuda.h
 	mkdir -p $(PKG)/lib
-	$(NVCC) $(NVFLAGS) -o $@ $(CSRC)/ngemm_cuda.cu -lcudart
+	$(NVCC) $(NVFLAGS) -o $@ $(CSRC)/ngemm_cuda.cu
 
 oracle:
 	$(MAKE) -s -C oracle

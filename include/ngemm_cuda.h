@@ -65,7 +65,9 @@ typedef enum {
     NGEMM_KERNEL_SKINNY = 3   /* memory-bound M <= 16 path, both modes */
 } ngemm_kernel;
 
-/* PackedWeight metadata (layout.hpp:120-135; NGPT trailer layout.hpp:283-293). */
+/* PackedWeight metadata (layout.hpp:120-135; NGPT trailer layout.hpp:283-293).  h = 4 is the
+ * u8 path (1-byte elements), h = 2 the i16 path (2-byte elements); packed byte size is
+ * m_pad * k_pad * element size. */
 typedef struct {
     int32_t w, h, v;      /* KernelShape */
     int64_t tm, tn, tk;   /* TileConfig */
@@ -117,9 +119,25 @@ ngemm_status ngemm_cuda_gemm_packed(ngemm_packed_handle h, const int8_t* b, int6
 
 ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_t* c, int64_t m,
                                        int64_t n, int64_t k, int sat_mode, int kernel);
+/* Packed weight + input, host pointers; the weight kind follows meta->h (4: u8 weight with i8 b,
+ * 2: i16 weight with i16 b; the 16-bit path has no saturation stage, gemm.hpp:161-190). */
 ngemm_status ngemm_cuda_gemm_packed_host(const ngemm_packed_meta* meta, const uint8_t* host_packed,
-                                         size_t nbytes, const int8_t* b, int32_t* c, int64_t n,
+                                         size_t nbytes, const void* b, int32_t* c, int64_t n,
                                          int sat_mode, int kernel);
+
+/* Device-resident weight handle + HOST input B and output C (what gemm_ngemm calls: the weight
+ * stays on the device across calls, B and C cross the bus per call). */
+ngemm_status ngemm_cuda_gemm_packed_resident_host(ngemm_packed_handle h, const int8_t* b, int32_t* c,
+                                                  int64_t n, int sat_mode);
+
+/* ---- the reference's 16-bit path: i16 x i16 -> i32 (gemm.hpp:161-190, 245-281;
+ * madd_pair_i16 wraps mod 2^32, lanes.hpp:42-47).  CUDA-core kernel; lda/ldb in elements. */
+ngemm_status ngemm_cuda_gemm_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c,
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream);
+ngemm_status ngemm_cuda_gemm_i16_host(const int16_t* a, const int16_t* b, int32_t* c, int64_t m, int64_t n,
+                                      int64_t k);
+ngemm_status ngemm_cuda_gemm_packed_i16(ngemm_packed_handle h, const int16_t* b, int64_t ldb, int32_t* c,
+                                        int64_t ldc, int64_t n, void* stream);
 
 /* ---- multi-GPU M-shard driver (single process, one stream per device) -------------------
  * A's rows are split into ndev contiguous, tile-aligned blocks; B is replicated; device d
@@ -133,6 +151,8 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
 ngemm_status ngemm_cuda_free(void* device_ptr);
 
 /* ---- introspection ----------------------------------------------------------------------- */
+/* Current CUDA device of the calling thread. */
+ngemm_status ngemm_cuda_device(int* device);
 int ngemm_cuda_abi_version(void);
 const char* ngemm_cuda_status_name(int status);
 /* Thread-local message of the last failing call on this thread ("" if none). */

@@ -19,7 +19,8 @@ EXPORTS = [
     "ngemm_cuda_packed_info", "ngemm_cuda_gemm_packed", "ngemm_cuda_gemm_u8i8_host",
     "ngemm_cuda_gemm_packed_host", "ngemm_cuda_shard_rows", "ngemm_cuda_gemm_u8i8_multi", "ngemm_cuda_free",
     "ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error", "ngemm_cuda_pick_kernel",
-    "ngemm_cuda_launch_count",
+    "ngemm_cuda_launch_count", "ngemm_cuda_gemm_i16", "ngemm_cuda_gemm_i16_host", "ngemm_cuda_gemm_packed_i16",
+    "ngemm_cuda_gemm_packed_resident_host", "ngemm_cuda_device",
 ]
 
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA = range(8)
@@ -65,6 +66,11 @@ def load():
         L.ngemm_cuda_gemm_u8i8_multi.argtypes = [C.POINTER(i32), i32, vp, vp, vp, i64, i64, i64, i32, i32,
                                                  C.POINTER(vp)]
         L.ngemm_cuda_free.argtypes = [vp]
+        L.ngemm_cuda_gemm_i16.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp]
+        L.ngemm_cuda_gemm_i16_host.argtypes = [vp, vp, vp, i64, i64, i64]
+        L.ngemm_cuda_gemm_packed_i16.argtypes = [vp, vp, i64, vp, i64, i64, vp]
+        L.ngemm_cuda_gemm_packed_resident_host.argtypes = [vp, vp, vp, i64, i32]
+        L.ngemm_cuda_device.argtypes = [C.POINTER(i32)]
         for f in EXPORTS:
             fn = getattr(L, f)
             if f not in ("ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error",

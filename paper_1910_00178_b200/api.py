@@ -184,7 +184,9 @@ def _engine_kernel(engine: Engine) -> int:
 
 
 def _check_operands(a: np.ndarray, b: np.ndarray):  # gemm.hpp:19-30
-    if a.dtype != np.uint8 or b.dtype != np.int8:
+    u8i8 = a.dtype == np.uint8 and b.dtype == np.int8
+    i16 = a.dtype == np.int16 and b.dtype == np.int16
+    if not (u8i8 or i16):
         raise UnsupportedError(f"gemm: no kernel path for {a.dtype} x {b.dtype}")
     if a.ndim != 2 or b.ndim != 2 or a.shape[1] != b.shape[1]:
         raise ShapeError(f"gemm: K mismatch, A is {a.shape} but B is {b.shape} (B is stored [N x K])")
@@ -196,12 +198,15 @@ def gemm_conventional(a: np.ndarray, b: np.ndarray, shape: KernelShape, mode: Sa
     a = np.ascontiguousarray(a)
     b = np.ascontiguousarray(b)
     _check_operands(a, b)
-    if shape.v * shape.h != shape.w or shape.h != 4:
+    if shape.v * shape.h != shape.w or shape.h != (4 if a.dtype == np.uint8 else 2):
         raise ShapeError("gemm_conventional: kernel shape does not match operand kind")
     kernel = _engine_kernel(engine)
     m, k = a.shape
     n = b.shape[0]
     c = np.empty((m, n), np.int32)
+    if a.dtype == np.int16:  # the 16-bit path has no saturation stage (gemm.hpp:161-190)
+        check(_lib.load().ngemm_cuda_gemm_i16_host(a.ctypes.data, b.ctypes.data, c.ctypes.data, m, n, k))
+        return c
     check(_lib.load().ngemm_cuda_gemm_u8i8_host(a.ctypes.data, b.ctypes.data, c.ctypes.data, m, n, k, int(mode),
                                                   kernel))
     return c

@@ -17,7 +17,7 @@ struct PackedGeom {
     int64_t tm, tk, m_pad, k_pad, m_orig, k_orig;
 };
 
-// PackedWeight::block_offset (layout.hpp:152-165) in bytes for 8-bit elements.
+// PackedWeight::block_offset (layout.hpp:152-165), in elements.
 __device__ __forceinline__ int64_t packed_block_offset(const PackedGeom& g, int64_t m_blk, int64_t k_blk) {
     const int64_t tile_m = m_blk * g.v / g.tm;
     const int64_t tile_k = k_blk * g.h / g.tk;
@@ -30,23 +30,25 @@ __device__ __forceinline__ int64_t packed_block_offset(const PackedGeom& g, int6
     return (tile_lin * blocks_per_tile + bm * (g.tk / g.h) + bk) * g.w;
 }
 
-// One thread per (row gm, K-word kw) of the output; a warp covers 32 consecutive K-words of
-// one row, so the row-major writes are coalesced; the packed reads of consecutive K-words of a
-// row are w bytes apart inside a tile and hit L2 lines that neighbouring rows reuse.
+// One thread per (row gm, 4-byte K-group kw) of the output; a warp covers 32 consecutive
+// K-groups of one row, so the row-major writes are coalesced; the packed reads of consecutive
+// K-groups of a row are w elements apart inside a tile and hit L2 lines that neighbouring rows
+// reuse.  esize = 1 (u8, h = 4) or 2 (i16, h = 2): a K-group is always one 4-byte word.
 __global__ void repack_kernel(PackedGeom g, const uint8_t* __restrict__ packed, uint8_t* __restrict__ a,
-                              int64_t lda, int64_t kwords) {
+                              int64_t lda_bytes, int64_t kwords, int esize) {
     const int64_t total = g.m_orig * kwords;
+    const int64_t k_bytes = g.k_orig * esize;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t gm = i / kwords, kw = i - gm * kwords;
-        const int64_t gk = kw * 4;
-        const int64_t off = packed_block_offset(g, gm / g.v, kw) + (gm % g.v) * 4;
+        const int64_t off = (packed_block_offset(g, gm / g.v, kw) + (gm % g.v) * g.h) * esize;
         const uint32_t word = *reinterpret_cast<const uint32_t*>(packed + off);
-        uint8_t* dst = a + gm * lda + gk;
-        if (gk + 4 <= g.k_orig && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
+        const int64_t gb = kw * 4;  // byte position in the row
+        uint8_t* dst = a + gm * lda_bytes + gb;
+        if (gb + 4 <= k_bytes && ((reinterpret_cast<uintptr_t>(dst) & 3) == 0)) {
             *reinterpret_cast<uint32_t*>(dst) = word;
         } else {
-            for (int q = 0; q < 4 && gk + q < g.k_orig; ++q) dst[q] = static_cast<uint8_t>(word >> (8 * q));
+            for (int q = 0; q < 4 && gb + q < k_bytes; ++q) dst[q] = static_cast<uint8_t>(word >> (8 * q));
         }
     }
 }

@@ -39,7 +39,10 @@ __device__ __forceinline__ uint4 simt_load16(const uint8_t* __restrict__ base, i
     return make_uint4(w[0], w[1], w[2], w[3]);
 }
 
-template <int MODE>  // 1 = WideningExact, 0 = HardwareSaturating
+// MODE: 1 = WideningExact, 0 = HardwareSaturating (u8 x s8 words of 4 K-elements);
+//       2 = the 16-bit path, i16 x i16 words of 2 K-elements (madd_pair_i16, lanes.hpp:42-47:
+//           no saturation stage, everything mod 2^32).  K, lda, ldb are in BYTES here.
+template <int MODE>
 __global__ void __launch_bounds__(simt::THREADS, 2)
     simt_gemm_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                      int32_t* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int vec_ok,
@@ -99,6 +102,18 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
                 for (int i = 0; i < 8; ++i)
 #pragma unroll
                     for (int j = 0; j < 8; ++j) acc[i][j] = dp4a_us(a[i], b[j], acc[i][j]);
+            } else if constexpr (MODE == 2) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) {
+                    const int32_t alo = static_cast<int16_t>(a[i] & 0xFFFFu), ahi = static_cast<int32_t>(a[i]) >> 16;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int32_t blo = static_cast<int16_t>(b[j] & 0xFFFFu), bhi = static_cast<int32_t>(b[j]) >> 16;
+                        acc[i][j] = static_cast<int32_t>(static_cast<uint32_t>(acc[i][j]) +
+                                                         static_cast<uint32_t>(alo * blo) +
+                                                         static_cast<uint32_t>(ahi * bhi));
+                    }
+                }
             } else {
 #pragma unroll
                 for (int i = 0; i < 8; ++i) {

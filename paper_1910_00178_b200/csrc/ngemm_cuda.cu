@@ -175,6 +175,22 @@ ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t
     return NGEMM_OK;
 }
 
+// i16 x i16 -> i32 (the reference's 16-bit path, gemm.hpp:161-190, 245-281): SIMT kernel in
+// MODE 2 over the operands viewed as bytes (2 bytes per element, K-groups of 2 per word).
+ngemm_status launch_simt_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                             int64_t m, int64_t n, int64_t k, cudaStream_t st) {
+    const uint8_t* ab = reinterpret_cast<const uint8_t*>(a);
+    const int8_t* bb = reinterpret_cast<const int8_t*>(b);
+    const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
+                        (lda * 2) % 16 == 0 && (ldb * 2) % 16 == 0);
+    const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
+    dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
+    if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
+    simt_gemm_kernel<2><<<grid, simt::THREADS, 0, st>>>(ab, lda * 2, bb, ldb * 2, c, ldc, m, n, k * 2, vec_ok, c_vec);
+    NG_LAUNCHED();
+    return NGEMM_OK;
+}
+
 constexpr int kSkinnyMaxM = 16;
 constexpr int64_t kSkinnySmemCap = 200 * 1024;
 
@@ -349,9 +365,9 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
 // ---------------------------------------------------------------- packed weights
 ngemm_status validate_meta(const ngemm_packed_meta* p) {
     if (!p) return fail(NGEMM_ERR_CONFIG, "null packed metadata");
-    if (p->v * p->h != p->w || p->h != 4)
+    if (p->v * p->h != p->w || (p->h != 4 && p->h != 2) || p->v < 1)
         return fail(NGEMM_ERR_CONFIG, "pack: shape (w=" + std::to_string(p->w) + ",h=" + std::to_string(p->h) +
-                                          ",v=" + std::to_string(p->v) + ") does not match the u8 path");
+                                          ",v=" + std::to_string(p->v) + ") matches neither the u8 (h=4) nor the i16 (h=2) path");
     if (p->tm < p->v || p->tm % p->v != 0)
         return fail(NGEMM_ERR_CONFIG, "tile: tm=" + std::to_string(p->tm) + " is not a positive multiple of v");
     if (p->tk < p->h || p->tk % p->h != 0)
@@ -385,10 +401,12 @@ ngemm_status repack_on(const ngemm_packed_meta* meta, const uint8_t* d_packed, u
     if (s != NGEMM_OK) return s;
     if (lda < meta->k_orig) return fail(NGEMM_ERR_SHAPE, "repack: lda < K");
     if (reinterpret_cast<uintptr_t>(d_packed) % 4 != 0) return fail(NGEMM_ERR_SHAPE, "repack: packed buffer must be 4-byte aligned");
-    const int64_t kwords = (meta->k_orig + 3) / 4;
+    const int esize = meta->h == 4 ? 1 : 2;  // K-group of h elements = one 4-byte word
+    const int64_t kwords = (meta->k_orig + meta->h - 1) / meta->h;
     const int64_t total = meta->m_orig * kwords;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
-    repack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(geom_of(meta), d_packed, d_a, lda, kwords);
+    repack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(geom_of(meta), d_packed, d_a, lda * esize, kwords,
+                                                                 esize);
     NG_LAUNCHED();
     return NGEMM_OK;
 }
@@ -398,8 +416,69 @@ ngemm_status repack_on(const ngemm_packed_meta* meta, const uint8_t* d_packed, u
 struct ngemm_packed_dev {
     int device;
     uint8_t* d_a;
-    int64_t lda, m, k;
+    int64_t lda, m, k;  // lda and k in elements
+    int esize;          // 1 = u8 weight (u8 x i8 path), 2 = i16 weight (16-bit path)
 };
+
+namespace {
+
+ngemm_status run_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc, int64_t m,
+                     int64_t n, int64_t k, cudaStream_t st) {
+    ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, NGEMM_SAT_EXACT);
+    if (s != NGEMM_OK) return s;
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    return launch_simt_i16(a, lda, b, ldb, c, ldc, m, n, k, st);
+}
+
+// Host operands -> pooled device buffers (rows padded to 16 bytes for TMA) -> optional device
+// repack of a packed weight -> GEMM -> host C.  esize selects the u8 x i8 or i16 x i16 path.
+ngemm_status host_gemm(int esize, const ngemm_packed_meta* meta, const void* a_or_packed, size_t packed_bytes,
+                       const void* b, int32_t* c, int64_t m, int64_t n, int64_t k, int sat_mode, int kernel) {
+    int dev;
+    DevInfo di;
+    ngemm_status s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    const int64_t kb = k * esize;            // row bytes
+    const int64_t kpb = round_up(kb, 16);    // padded row bytes
+    const int64_t kp = kpb / esize;          // padded row elements
+    const size_t p_bytes = meta ? packed_bytes : 0;
+    const size_t a_bytes = static_cast<size_t>(m * kpb), b_bytes = static_cast<size_t>(n * kpb);
+    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
+    const size_t a_off = round_up(static_cast<int64_t>(p_bytes), 256), b_off = a_off + round_up(a_bytes, 256),
+                 c_off = b_off + round_up(b_bytes, 256);
+    cudaStream_t st = nullptr;
+    uint8_t* buf = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
+    bool ok = true;
+    if (meta) {
+        ok = cudaMemcpyAsync(buf, a_or_packed, p_bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
+    } else {
+        ok = copy_rows_h2d(buf + a_off, kpb, a_or_packed, kb, m, st) == cudaSuccess;
+    }
+    ok = ok && copy_rows_h2d(buf + b_off, kpb, b, kb, n, st) == cudaSuccess;
+    s = ok ? NGEMM_OK : fail(NGEMM_ERR_CUDA, "host gemm: H2D copy failed");
+    if (s == NGEMM_OK && meta) s = repack_on(meta, buf, buf + a_off, kp, st);
+    if (s == NGEMM_OK) {
+        int32_t* dc = reinterpret_cast<int32_t*>(buf + c_off);
+        if (esize == 1)
+            s = run_gemm(buf + a_off, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp, dc, n, m, n, k, sat_mode,
+                         kernel, st);
+        else
+            s = run_i16(reinterpret_cast<const int16_t*>(buf + a_off), kp,
+                        reinterpret_cast<const int16_t*>(buf + b_off), kp, dc, n, m, n, k, st);
+    }
+    if (s == NGEMM_OK && cudaMemcpyAsync(c, buf + c_off, c_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
+        s = fail(NGEMM_ERR_CUDA, "host gemm: D2H copy failed");
+    cudaFreeAsync(buf, st);
+    if (cudaStreamSynchronize(st) != cudaSuccess && s == NGEMM_OK)
+        s = fail(NGEMM_ERR_CUDA, std::string("host gemm: ") + cudaGetErrorString(cudaGetLastError()));
+    return s;
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -443,28 +522,36 @@ ngemm_status ngemm_cuda_repack(const ngemm_packed_meta* meta, const uint8_t* d_p
     return repack_on(meta, d_packed, d_a, lda, static_cast<cudaStream_t>(stream));
 }
 
+
+ngemm_status ngemm_cuda_gemm_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c,
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, void* stream) {
+    return run_i16(a, lda, b, ldb, c, ldc, m, n, k, static_cast<cudaStream_t>(stream));
+}
+
 ngemm_status ngemm_cuda_packed_upload(const ngemm_packed_meta* meta, const uint8_t* host_packed, size_t nbytes,
                                       ngemm_packed_handle* out) {
     ngemm_status s = validate_meta(meta);
     if (s != NGEMM_OK) return s;
     if (!out || !host_packed) return fail(NGEMM_ERR_SHAPE, "packed_upload: null pointer");
-    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad))
+    const int esize = meta->h == 4 ? 1 : 2;
+    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad * esize))
         return fail(NGEMM_ERR_SHAPE, "packed_upload: byte size disagrees with m_pad*k_pad");
     int dev;
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    const int64_t lda = round_up(meta->k_orig, 16);
+    const int64_t lda = round_up(meta->k_orig * esize, 16) / esize;
+    const size_t a_bytes = static_cast<size_t>(meta->m_orig * lda * esize);
     uint8_t* d_packed = nullptr;
     uint8_t* d_a = nullptr;
     NG_CUDA(cudaMalloc(&d_packed, nbytes));
-    if (cudaMalloc(&d_a, static_cast<size_t>(meta->m_orig * lda)) != cudaSuccess) {
+    if (cudaMalloc(&d_a, a_bytes) != cudaSuccess) {
         cudaFree(d_packed);
         return fail(NGEMM_ERR_CUDA, "packed_upload: out of device memory");
     }
     cudaStream_t st = nullptr;
     s = NGEMM_OK;
-    if (cudaMemsetAsync(d_a, 0, static_cast<size_t>(meta->m_orig * lda), st) != cudaSuccess ||
+    if (cudaMemsetAsync(d_a, 0, a_bytes, st) != cudaSuccess ||
         cudaMemcpyAsync(d_packed, host_packed, nbytes, cudaMemcpyHostToDevice, st) != cudaSuccess)
         s = fail(NGEMM_ERR_CUDA, "packed_upload: copy failed");
     if (s == NGEMM_OK) s = repack_on(meta, d_packed, d_a, lda, st);
@@ -474,7 +561,7 @@ ngemm_status ngemm_cuda_packed_upload(const ngemm_packed_meta* meta, const uint8
         cudaFree(d_a);
         return s;
     }
-    *out = new ngemm_packed_dev{dev, d_a, lda, meta->m_orig, meta->k_orig};
+    *out = new ngemm_packed_dev{dev, d_a, lda, meta->m_orig, meta->k_orig, esize};
     return NGEMM_OK;
 }
 
@@ -494,7 +581,7 @@ ngemm_status ngemm_cuda_packed_from_device(const uint8_t* d_src, int64_t lda_src
         cudaFree(d_a);
         return fail(NGEMM_ERR_CUDA, "packed_from_device: copy failed");
     }
-    *out = new ngemm_packed_dev{dev, d_a, lda, m, k};
+    *out = new ngemm_packed_dev{dev, d_a, lda, m, k, 1};
     return NGEMM_OK;
 }
 
@@ -523,8 +610,17 @@ ngemm_status ngemm_cuda_packed_info(ngemm_packed_handle h, const uint8_t** d_a, 
 ngemm_status ngemm_cuda_gemm_packed(ngemm_packed_handle h, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                                     int64_t n, int sat_mode, void* stream) {
     if (!h) return fail(NGEMM_ERR_SHAPE, "null handle");
+    if (h->esize != 1) return fail(NGEMM_ERR_UNSUPPORTED, "gemm_packed: i16 weight needs an i16 input (gemm_packed_i16)");
     return run_gemm(h->d_a, h->lda, b, ldb, c, ldc, h->m, n, h->k, sat_mode, NGEMM_KERNEL_AUTO,
                     static_cast<cudaStream_t>(stream));
+}
+
+ngemm_status ngemm_cuda_gemm_packed_i16(ngemm_packed_handle h, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                                        int64_t n, void* stream) {
+    if (!h) return fail(NGEMM_ERR_SHAPE, "null handle");
+    if (h->esize != 2) return fail(NGEMM_ERR_UNSUPPORTED, "gemm_packed_i16: u8 weight needs an i8 input");
+    return run_i16(reinterpret_cast<const int16_t*>(h->d_a), h->lda, b, ldb, c, ldc, h->m, n, h->k,
+                   static_cast<cudaStream_t>(stream));
 }
 
 // ---------------------------------------------------------------- host-pointer entries
@@ -532,68 +628,63 @@ ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_
                                        int sat_mode, int kernel) {
     ngemm_status s = validate(a, k, b, k, c, n, m, n, k, sat_mode);
     if (s != NGEMM_OK) return s;
+    return host_gemm(1, nullptr, a, 0, b, c, m, n, k, sat_mode, kernel);
+}
+
+ngemm_status ngemm_cuda_gemm_packed_resident_host(ngemm_packed_handle h, const int8_t* b, int32_t* c, int64_t n,
+                                                  int sat_mode) {
+    if (!h) return fail(NGEMM_ERR_SHAPE, "null handle");
+    if (h->esize != 1) return fail(NGEMM_ERR_UNSUPPORTED, "gemm_packed_resident_host: u8 weights only");
+    ngemm_status s = validate(h->d_a, h->lda, b, h->k, c, n, h->m, n, h->k, sat_mode);
+    if (s != NGEMM_OK) return s;
     int dev;
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    const int64_t kp = round_up(k, 16);
-    uint8_t* buf = nullptr;
-    const size_t a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
-    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
-    const size_t a_off = 0, b_off = round_up(a_bytes, 256), c_off = b_off + round_up(b_bytes, 256);
+    if (dev != h->device) return fail(NGEMM_ERR_UNSUPPORTED, "weight handle lives on another device");
+    const int64_t k = h->k, m = h->m, kp = round_up(k, 16);
+    const size_t b_bytes = static_cast<size_t>(n * kp), c_bytes = static_cast<size_t>(m * n) * 4;
+    const size_t c_off = round_up(b_bytes, 256);
     cudaStream_t st = nullptr;
+    uint8_t* buf = nullptr;
     NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
-    s = NGEMM_OK;
-    if (copy_rows_h2d(buf + a_off, kp, a, k, m, st) != cudaSuccess ||
-        copy_rows_h2d(buf + b_off, kp, b, k, n, st) != cudaSuccess)
-        s = fail(NGEMM_ERR_CUDA, "gemm_host: H2D copy failed");
+    s = copy_rows_h2d(buf, kp, b, k, n, st) == cudaSuccess ? NGEMM_OK : fail(NGEMM_ERR_CUDA, "H2D copy failed");
     if (s == NGEMM_OK)
-        s = run_gemm(buf + a_off, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
-                     reinterpret_cast<int32_t*>(buf + c_off), n, m, n, k, sat_mode,
-                     kernel, st);
+        s = run_gemm(h->d_a, h->lda, reinterpret_cast<const int8_t*>(buf), kp, reinterpret_cast<int32_t*>(buf + c_off),
+                     n, m, n, k, sat_mode, NGEMM_KERNEL_AUTO, st);
     if (s == NGEMM_OK && cudaMemcpyAsync(c, buf + c_off, c_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        s = fail(NGEMM_ERR_CUDA, "gemm_host: D2H copy failed");
+        s = fail(NGEMM_ERR_CUDA, "D2H copy failed");
     cudaFreeAsync(buf, st);
     if (cudaStreamSynchronize(st) != cudaSuccess && s == NGEMM_OK)
-        s = fail(NGEMM_ERR_CUDA, std::string("gemm_host: ") + cudaGetErrorString(cudaGetLastError()));
+        s = fail(NGEMM_ERR_CUDA, std::string("gemm_packed_resident_host: ") + cudaGetErrorString(cudaGetLastError()));
     return s;
 }
 
+ngemm_status ngemm_cuda_device(int* device) {
+    if (!device) return fail(NGEMM_ERR_SHAPE, "null pointer");
+    NG_CUDA(cudaGetDevice(device));
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_gemm_i16_host(const int16_t* a, const int16_t* b, int32_t* c, int64_t m, int64_t n,
+                                      int64_t k) {
+    ngemm_status s = validate(a, k, b, k, c, n, m, n, k, NGEMM_SAT_EXACT);
+    if (s != NGEMM_OK) return s;
+    return host_gemm(2, nullptr, a, 0, b, c, m, n, k, NGEMM_SAT_EXACT, NGEMM_KERNEL_SIMT);
+}
+
 ngemm_status ngemm_cuda_gemm_packed_host(const ngemm_packed_meta* meta, const uint8_t* host_packed, size_t nbytes,
-                                         const int8_t* b, int32_t* c, int64_t n, int sat_mode, int kernel) {
+                                         const void* b, int32_t* c, int64_t n, int sat_mode, int kernel) {
     ngemm_status s = validate_meta(meta);
     if (s != NGEMM_OK) return s;
-    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad))
+    const int esize = meta->h == 4 ? 1 : 2;
+    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad * esize))
         return fail(NGEMM_ERR_SHAPE, "gemm_packed_host: byte size disagrees with m_pad*k_pad");
     const int64_t m = meta->m_orig, k = meta->k_orig;
-    s = validate(host_packed, k, b, k, c, n, m, n, k, sat_mode);
+    s = validate(host_packed, k, b, k, c, n, m, n, k, esize == 1 ? sat_mode : NGEMM_SAT_EXACT);
     if (s != NGEMM_OK) return s;
-    int dev;
-    DevInfo di;
-    s = current_device(&dev, &di);
-    if (s != NGEMM_OK) return s;
-    const int64_t kp = round_up(k, 16);
-    const size_t p_bytes = nbytes, a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
-    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
-    const size_t p_off = 0, a_off = round_up(p_bytes, 256), b_off = a_off + round_up(a_bytes, 256),
-                 c_off = b_off + round_up(b_bytes, 256);
-    cudaStream_t st = nullptr;
-    uint8_t* buf = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
-    s = NGEMM_OK;
-    if (cudaMemcpyAsync(buf + p_off, host_packed, p_bytes, cudaMemcpyHostToDevice, st) != cudaSuccess ||
-        copy_rows_h2d(buf + b_off, kp, b, k, n, st) != cudaSuccess)
-        s = fail(NGEMM_ERR_CUDA, "gemm_packed_host: H2D copy failed");
-    if (s == NGEMM_OK) s = repack_on(meta, buf + p_off, buf + a_off, kp, st);
-    if (s == NGEMM_OK)
-        s = run_gemm(buf + a_off, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
-                     reinterpret_cast<int32_t*>(buf + c_off), n, m, n, k, sat_mode, kernel, st);
-    if (s == NGEMM_OK && cudaMemcpyAsync(c, buf + c_off, c_bytes, cudaMemcpyDeviceToHost, st) != cudaSuccess)
-        s = fail(NGEMM_ERR_CUDA, "gemm_packed_host: D2H copy failed");
-    cudaFreeAsync(buf, st);
-    if (cudaStreamSynchronize(st) != cudaSuccess && s == NGEMM_OK)
-        s = fail(NGEMM_ERR_CUDA, std::string("gemm_packed_host: ") + cudaGetErrorString(cudaGetLastError()));
-    return s;
+    return host_gemm(esize, meta, host_packed, nbytes, b, c, m, n, k, sat_mode,
+                     esize == 1 ? kernel : NGEMM_KERNEL_SIMT);
 }
 
 // ---------------------------------------------------------------- multi-GPU M-shard driver
