@@ -16,10 +16,11 @@
 //                 stage into a double-buffered TMEM accumulator; tcgen05.commit (multicast
 //                 to the pair) frees the stage in both CTAs and publishes finished tiles;
 //   warp 2      : TMEM allocator (cta_group::CG);
-//   warps 4..7  : epilogue — tcgen05.ld 32 lanes x 32 columns -> registers -> 128-byte row
-//                 segments of C, overlapped with the next tile's MMAs.
-// Split-K (splits > 1) writes through atomic adds on a zeroed C; integer wrap-add is
-// associative, so split-K is bit-exact.
+//   warps 4..7  : epilogue — tcgen05.ld 32 lanes x 32 columns -> registers -> smem -> TMA,
+//                 overlapped with the next tile's MMAs (double-buffered TMEM accumulator).
+//   C leaves through swizzled smem staging and TMA tensor stores (full 128-byte lines);
+//   split-K (splits > 1) uses the TMA unit's s32 reduce-add into a zeroed C — integer
+//   wrap-add is associative, so split-K is bit-exact.
 #pragma once
 
 #include "ptx.cuh"
@@ -40,9 +41,13 @@ struct Smem {
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
     static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
                                    : (2 * BN <= 256) ? 256 : 512;
-    static constexpr int BAR_OFFSET = STAGES * STAGE_BYTES;
+    // epilogue staging: 4 warps x 2 buffers x (32 rows x 32 int32) in SWIZZLE_128B order
+    static constexpr int STAGE_C_BYTES = 32 * 32 * 4;
+    static constexpr int C_OFFSET = STAGES * STAGE_BYTES;
+    static constexpr int BAR_OFFSET = C_OFFSET + 4 * 2 * STAGE_C_BYTES;
     static constexpr int BAR_BYTES = (2 * STAGES + 4) * 8 + 16;
     static constexpr int TOTAL = BAR_OFFSET + BAR_BYTES + 1024;  // +1024 for manual alignment
+    static_assert(TOTAL <= 232448, "exceeds the 227 KB opt-in shared memory per CTA");
 };
 }  // namespace tc
 
@@ -66,8 +71,10 @@ struct TileMap {
 template <int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                   int32_t* __restrict__ C, int64_t ldc, int M, int N, int num_kb_total, TileMap map,
-                   int c_vec_ok) {
+                   const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
+                   int num_kb_total, TileMap map, int c_mode) {
+    // c_mode: 0 = TMA tensor store of C (SWIZZLE_128B staging), 1 = TMA reduce-add into a
+    // zeroed C (split-K), 2 = direct 128-byte row-segment stores (C not TMA-describable).
     using S = tc::Smem<BN, STAGES, CG>;
     constexpr int UMMA_M = tc::BM * CG;
     extern __shared__ uint8_t smem_raw[];
@@ -88,6 +95,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
+        if (c_mode != 2) tma_prefetch(&tma_c);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -172,9 +180,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             }
         }
     } else if (warp >= 4) {
-        // ---------------- epilogue (both CTAs): TMEM -> registers -> global
+        // ---------------- epilogue (both CTAs): TMEM -> registers -> swizzled smem -> TMA store
         const int ew = warp & 3;  // TMEM lane quadrant this warp may access
-        int acc = 0;
+        uint8_t* stage_c = smem + S::C_OFFSET + ew * 2 * S::STAGE_C_BYTES;
+        int acc = 0, cbuf = 0;
         uint32_t acc_ph = 0;
         for (int t = unit; t < num_tiles; t += num_units) {
             int tm, tn, ks;
@@ -183,31 +192,41 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const bool has_k = kb0 < num_kb_total;
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
-            const int64_t row = static_cast<int64_t>(tm) * UMMA_M + rank * tc::BM + ew * 32 + lane;
+            const int row0 = tm * UMMA_M + static_cast<int>(rank) * tc::BM + ew * 32;
             const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
-            int32_t* crow = C + row * ldc;
 #pragma unroll 1
             for (int c = 0; c < BN; c += 32) {
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(taddr + c, v);
                 tmem_wait_ld();
-                if (!has_k || row >= M) continue;
-                const int64_t col0 = static_cast<int64_t>(tn) * BN + c;
-                if (map.splits == 1) {
-                    if (c_vec_ok && col0 + 32 <= N) {
+                if (!has_k || row0 >= M) continue;
+                const int col0 = tn * BN + c;
+                if (c_mode != 2) {
+                    uint8_t* buf = stage_c + cbuf * S::STAGE_C_BYTES;
+                    // the TMA store that last read this buffer must be done with it
+                    if (lane == 0) tma_store_wait_read<1>();
+                    __syncwarp();
+                    const uint32_t rowp = smem_u32(buf) + lane * 128;
 #pragma unroll
-                        for (int q = 0; q < 8; ++q)
-                            *reinterpret_cast<int4*>(crow + col0 + 4 * q) =
-                                make_int4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-                    } else {
+                    for (int j = 0; j < 8; ++j)
+                        st_shared_v4(rowp + ((j ^ (lane & 7)) << 4), v[4 * j], v[4 * j + 1], v[4 * j + 2],
+                                     v[4 * j + 3]);
+                    fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (c_mode == 0) tma_store_2d(&tma_c, buf, col0, row0);
+                        else tma_reduce_add_2d(&tma_c, buf, col0, row0);
+                        tma_store_commit();
+                    }
+                    cbuf ^= 1;
+                } else {
+                    const int64_t row = static_cast<int64_t>(row0) + lane;
+                    if (row < M) {
+                        int32_t* crow = C + row * ldc;
 #pragma unroll
                         for (int q = 0; q < 32; ++q)
                             if (col0 + q < N) crow[col0 + q] = static_cast<int32_t>(v[q]);
                     }
-                } else {
-#pragma unroll
-                    for (int q = 0; q < 32; ++q)
-                        if (col0 + q < N) atomicAdd(reinterpret_cast<unsigned int*>(crow + col0 + q), v[q]);
                 }
             }
             tc_fence_before();
@@ -219,6 +238,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             acc ^= 1;
             if (acc == 0) acc_ph ^= 1;
         }
+        if (lane == 0) tma_store_wait<0>();
     }
 
     tc_fence_before();

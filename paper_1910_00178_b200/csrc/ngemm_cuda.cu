@@ -237,9 +237,72 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
                                    : launch_skinny_mode<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
 }
 
+// 2-D int32 C [rows x cols] with row stride ldc elements, 32 x 32 boxes, SWIZZLE_128B (the
+// epilogue's staging layout).
+ngemm_status make_tmap_c(CUtensorMap* map, const int32_t* c, int64_t rows, int64_t cols, int64_t ldc) {
+    EncodeTiledFn fn = encode_fn();
+    if (!fn) return fail(NGEMM_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ldc) * 4};
+    cuuint32_t box[2] = {32, 32};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int32_t*>(c), dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(NGEMM_ERR_CUDA, "cuTensorMapEncodeTiled(C) failed: " + std::to_string(r));
+    return NGEMM_OK;
+}
+
+// Tile configurations of the tcgen05 kernel (per CTA: 128 rows of A; cta_group::2 pairs two SMs).
+enum TcCfg { TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_NUM_CFG = 4 };
+struct TcCfgInfo {
+    int cg, bn;
+    double cycles_per_kb;  // MMA issue floor per 128-byte K slab, with the smem-bandwidth cap
+};
+constexpr TcCfgInfo kTcCfg[TC_NUM_CFG] = {
+    {2, 256, 512.0},  // 256x256x128 int8 per pair at 8192 MAC/clk/SM
+    {1, 256, 520.0},  // 128x256: 96 B/clk of smem operand reads
+    {1, 128, 300.0},  // 128x128: 128 B/clk, at the smem port limit
+    {1, 64, 192.0},   // 128x64 : smem-bound (192 B/clk needed)
+};
+
+struct TcPlan {
+    int cfg, splits;
+};
+
+// Picks the configuration with the smallest estimated makespan (waves x K-loop + epilogue),
+// then adds split-K (TMA reduce-add) while waves stay under one and K is deep.
+TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
+    const int64_t num_kb = (k + tc::BK - 1) / tc::BK;
+    TcPlan best{TC_PAIR256, 1};
+    double best_t = 1e30;
+    for (int cfg = 0; cfg < TC_NUM_CFG; ++cfg) {
+        const TcCfgInfo& ci = kTcCfg[cfg];
+        const int64_t tiles = ((m + 128 * ci.cg - 1) / (128 * ci.cg)) * ((n + ci.bn - 1) / ci.bn);
+        const int64_t units = sms / ci.cg;
+        for (int splits = 1; splits <= 16; splits *= 2) {
+            if (splits > 1 && (!c_mode_ok || num_kb < 4 * splits || tiles * splits > units)) break;
+            const int64_t work = tiles * splits;
+            const int64_t waves = (work + units - 1) / units;
+            const double kb = static_cast<double>((num_kb + splits - 1) / splits);
+            double t = static_cast<double>(waves) * kb * ci.cycles_per_kb + 600.0 + ci.bn * 8.0;
+            if (splits > 1) t += 1500.0;                 // zeroing C + reduce-add traffic
+            if (ci.cg == 2) t *= 0.97;                    // less L2->SM traffic per MAC
+            if (t < best_t) {
+                best_t = t;
+                best = {cfg, splits};
+            }
+        }
+    }
+    if (const char* force = std::getenv("NGEMM_TC_CFG")) best.cfg = std::atoi(force) % TC_NUM_CFG;  // experiments
+    if (const char* force = std::getenv("NGEMM_TC_SPLITS")) best.splits = std::max(1, std::atoi(force));
+    return best;
+}
+
 template <int BN, int STAGES, int CG>
-ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, int32_t* c, int64_t ldc, int64_t m,
-                         int64_t n, int64_t k, int splits_hint, const DevInfo& di, cudaStream_t st) {
+ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcmap, int32_t* c,
+                         int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int c_mode, const DevInfo& di,
+                         cudaStream_t st) {
     using S = tc::Smem<BN, STAGES, CG>;
     auto kern = tc_gemm_kernel<BN, STAGES, CG>;
     static std::once_flag once[64];
@@ -254,18 +317,16 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, int32_t* 
     const int num_kb = static_cast<int>((k + tc::BK - 1) / tc::BK);
     const int tiles = map.tiles_m * map.tiles_n;
     const int units = di.sms / CG;
-    int splits = 1;
-    if (splits_hint > 0) splits = std::min(splits_hint, num_kb);
-    else if (tiles * 2 <= units && num_kb >= 8) splits = std::max(1, std::min(num_kb / 4, units / tiles));
-    map.splits = splits;
+    // split-K needs the TMA reduce-add epilogue (C must be TMA-describable)
+    map.splits = c_mode == 2 ? 1 : std::max(1, std::min(splits, num_kb));
     map.group_m = tc::GROUP_M;
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
-    if (splits > 1) {
+    if (map.splits > 1) {
+        c_mode = 1;
         if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
         else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
     }
-    const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
-    const int grid = std::min(tiles * splits, units) * CG;
+    const int grid = std::min(tiles * map.splits, units) * CG;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(tc::THREADS);
@@ -278,8 +339,8 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, int32_t* 
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    NG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, c, ldc, static_cast<int>(m), static_cast<int>(n), num_kb, map,
-                               c_vec));
+    NG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcmap, c, ldc, static_cast<int>(m), static_cast<int>(n), num_kb,
+                               map, c_mode));
     NG_LAUNCHED();
     return NGEMM_OK;
 }
@@ -309,19 +370,22 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
             ldb_use = kp;
         }
     }
-    // Tile choice: 256 x 256 cta_group::2 pairs when there is enough work to fill the 74 SM
-    // pairs; otherwise single-CTA 128 x BN tiles (more tiles, plus split-K, for small shapes).
-    const int64_t tiles_pair = ((m + 255) / 256) * ((n + 255) / 256);
-    int cfg = (tiles_pair >= di.sms / 2) ? 2 : (n <= 128 ? 0 : 1);
-    if (const char* force = std::getenv("NGEMM_TC_CFG")) cfg = std::atoi(force) % 3;  // experiments only
-    const int bn_load = cfg == 2 ? 128 : (cfg == 0 ? 128 : 256);
-    CUtensorMap ta, tb;
+    const bool c_tma = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (ldc % 4 == 0);
+    const TcPlan plan = plan_tcgen05(m, n, k, di.sms, c_tma ? 1 : 0);
+    const TcCfgInfo& ci = kTcCfg[plan.cfg];
+    CUtensorMap ta, tb, tcm;
+    std::memset(&tcm, 0, sizeof tcm);
     ngemm_status s = make_tmap_u8(&ta, a_use, k, m, lda_use, tc::BK, tc::BM);
-    if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, bn_load);
+    if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, ci.bn / ci.cg);
+    if (s == NGEMM_OK && c_tma) s = make_tmap_c(&tcm, c, m, n, ldc);
+    const int c_mode = c_tma ? 0 : 2;
     if (s == NGEMM_OK) {
-        if (cfg == 2) s = launch_tc_t<256, 6, 2>(ta, tb, c, ldc, m, n, k, 0, di, st);
-        else if (cfg == 0) s = launch_tc_t<128, 6, 1>(ta, tb, c, ldc, m, n, k, 0, di, st);
-        else s = launch_tc_t<256, 4, 1>(ta, tb, c, ldc, m, n, k, 0, di, st);
+        switch (plan.cfg) {
+        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
+        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
+        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
+        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
+        }
     }
     if (scratch) cudaFreeAsync(scratch, st);
     return s;
