@@ -36,6 +36,8 @@ __device__ __forceinline__ int64_t packed_block_offset(const PackedGeom& g, int6
 // reuse.  esize = 1 (u8, h = 4) or 2 (i16, h = 2): a K-group is always one 4-byte word.
 __global__ void repack_kernel(PackedGeom g, const uint8_t* __restrict__ packed, uint8_t* __restrict__ a,
                               int64_t lda_bytes, int64_t kwords, int esize) {
+    pdl_launch_dependents();
+    pdl_wait();
     const int64_t total = g.m_orig * kwords;
     const int64_t k_bytes = g.k_orig * esize;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;

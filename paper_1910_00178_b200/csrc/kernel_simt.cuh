@@ -48,6 +48,8 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
                      int32_t* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int vec_ok,
                      int c_vec_ok) {
     using namespace simt;
+    pdl_launch_dependents();
+    pdl_wait();
     __shared__ __align__(16) uint32_t As[BKW][LDS];
     __shared__ __align__(16) uint32_t Bs[BKW][LDS];
 

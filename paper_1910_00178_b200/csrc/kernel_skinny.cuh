@@ -61,6 +61,8 @@ __global__ void __launch_bounds__(skinny::THREADS)
                        int b_vec_ok) {
     extern __shared__ __align__(16) uint8_t a_s[];  // [MT][kpad], zero padded
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_launch_dependents();
+    pdl_wait();
 
     // stage A (rows >= M and bytes >= K are zero)
     for (int64_t i = tid; i < static_cast<int64_t>(MT) * kpad; i += skinny::THREADS) {
@@ -137,6 +139,121 @@ __global__ void __launch_bounds__(skinny::THREADS)
                 const int64_t n = n0 + r;
                 if (m < M && n < N) C[static_cast<int64_t>(m) * ldc + n] = acc[i];
             }
+        }
+    }
+}
+
+}  // namespace ngemm_dev
+
+namespace ngemm_dev {
+
+// ---------------------------------------------------------------------------------------------
+// skinny_rows_kernel — the NGEMM broadcast idea on the GPU: every LANE owns one row of B (one
+// output column n) and accumulates all M outputs C[0..M)[n] in registers, while the matching
+// K-slice of A is BROADCAST to the warp from shared memory (one 16-byte wavefront serves all
+// 32 lanes).  No cross-lane reduction at all (the paper's phase-3 tree reduction disappears,
+// PAPER.md §3); the 8 warps of a CTA split the CTA's K range and meet once in shared memory.
+// B is read exactly once, 32 contiguous bytes (one full DRAM sector) per lane per step.
+// Grid: 32-row tiles of B x K splits; with K splits > 1 the partials are added into a zeroed C
+// (int32 wrap-add is order independent).  K splits start at multiples of 32 bytes, so
+// HardwareSaturating pairs stay even-aligned (gemm.hpp:94-99).
+// ---------------------------------------------------------------------------------------------
+namespace skinny_rows {
+constexpr int THREADS = 256;
+constexpr int WARPS = 8;
+constexpr int STEP = 32;  // bytes of K per lane per step
+}  // namespace skinny_rows
+
+template <int MODE, int MT>
+__global__ void __launch_bounds__(skinny_rows::THREADS)
+    skinny_rows_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
+                       int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range,
+                       int b_vec_ok, int accumulate) {
+    extern __shared__ __align__(16) uint8_t sm[];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    pdl_launch_dependents();
+    pdl_wait();
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 32;
+    const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
+    const int64_t kend = min(K, kbeg + k_range);
+    const int64_t span = ((kend - kbeg) + skinny_rows::STEP - 1) / skinny_rows::STEP * skinny_rows::STEP;
+
+    // A[0..MT) x [kbeg, kbeg+span) into smem, zero beyond M rows / K
+    uint8_t* a_s = sm;
+    for (int64_t i = tid; i < static_cast<int64_t>(MT) * span; i += skinny_rows::THREADS) {
+        const int64_t r = i / span, k = kbeg + (i - r * span);
+        a_s[i] = (r < M && k < kend) ? A[r * lda + k] : 0;
+    }
+    __syncthreads();
+
+    const int64_t n = n0 + lane;
+    const uint8_t* brow = reinterpret_cast<const uint8_t*>(B) + n * ldb;
+    int32_t acc[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) acc[m] = 0;
+
+    const int64_t steps = span / skinny_rows::STEP;
+#pragma unroll 2
+    for (int64_t s = warp; s < steps; s += skinny_rows::WARPS) {
+        const int64_t off = s * skinny_rows::STEP;  // within the CTA's K range
+        const int64_t k = kbeg + off;
+        uint32_t bw[8];
+        if (n < N && b_vec_ok && k + 32 <= kend) {
+            const uint4* p = reinterpret_cast<const uint4*>(brow + k);
+            uint4 v0, v1;
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v0.x), "=r"(v0.y), "=r"(v0.z), "=r"(v0.w) : "l"(p));
+            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(v1.x), "=r"(v1.y), "=r"(v1.z), "=r"(v1.w) : "l"(p + 1));
+            bw[0] = v0.x; bw[1] = v0.y; bw[2] = v0.z; bw[3] = v0.w;
+            bw[4] = v1.x; bw[5] = v1.y; bw[6] = v1.z; bw[7] = v1.w;
+        } else {
+#pragma unroll
+            for (int q = 0; q < 8; ++q) bw[q] = 0;
+            if (n < N) {
+#pragma unroll
+                for (int i = 0; i < 32; ++i)
+                    if (k + i < kend) bw[i >> 2] |= static_cast<uint32_t>(__ldg(brow + k + i)) << (8 * (i & 3));
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            const uint4 a0 = *reinterpret_cast<const uint4*>(a_s + m * span + off);       // broadcast
+            const uint4 a1 = *reinterpret_cast<const uint4*>(a_s + m * span + off + 16);  // broadcast
+            const uint32_t aw[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            int32_t sacc = acc[m];
+            if constexpr (MODE == 1) {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) sacc = dp4a_us(aw[q], bw[q], sacc);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 8; ++q) {
+                    const int32_t p0 = clamp_i16(dp4a_us(aw[q] & 0x0000FFFFu, bw[q], 0));
+                    const int32_t p1 = clamp_i16(dp4a_us(aw[q] & 0xFFFF0000u, bw[q], 0));
+                    sacc = static_cast<int32_t>(static_cast<uint32_t>(sacc) + static_cast<uint32_t>(p0) +
+                                                static_cast<uint32_t>(p1));
+                }
+            }
+            acc[m] = sacc;
+        }
+    }
+
+    // fold the 8 warps' partials: red[w][m][lane]
+    __syncthreads();
+    int32_t* red = reinterpret_cast<int32_t*>(sm);  // reuse the A staging area (>= 8*MT*32*4 bytes)
+#pragma unroll
+    for (int m = 0; m < MT; ++m) red[(warp * MT + m) * 32 + lane] = acc[m];
+    __syncthreads();
+    for (int i = tid; i < MT * 32; i += skinny_rows::THREADS) {
+        const int m = i >> 5, l = i & 31;
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < skinny_rows::WARPS; ++w) s += static_cast<uint32_t>(red[(w * MT + m) * 32 + l]);
+        const int64_t nn = n0 + l;
+        if (m < M && nn < N) {
+            int32_t* dst = C + static_cast<int64_t>(m) * ldc + nn;
+            if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
+            else *dst = static_cast<int32_t>(s);
         }
     }
 }

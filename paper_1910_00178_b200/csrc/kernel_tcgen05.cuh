@@ -92,6 +92,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int num_tiles = map.tiles_m * map.tiles_n * map.splits;
     const int kb_per_split = (num_kb_total + map.splits - 1) / map.splits;
 
+    pdl_launch_dependents();
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
@@ -111,6 +112,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if constexpr (CG == 2) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();  // operands / C may belong to the preceding kernel in the stream
 
     if (warp == 0) {
         if (lane == 0) {
@@ -246,6 +248,158 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, S::TMEM_COLS);
+    }
+}
+
+}  // namespace ngemm_dev
+
+namespace ngemm_dev {
+
+// ---------------------------------------------------------------------------------------------
+// tc_skinny_kernel — exact-mode skinny GEMM (M <= 16) on the tensor cores with the operands
+// swapped: D^T[n, m] = B[n, :] . A[m, :].  B's rows fill the UMMA M = 128 dimension and the
+// (zero-padded) A rows the UMMA N = 16 dimension, so no MMA work is wasted on padding M and
+// the kernel is a pure TMA stream over B: each CTA owns 128 rows of B and one K slice and
+// issues all of its TMA loads up front.  The KS CTAs that share a row tile form one thread-
+// block cluster along K; their 128 x 16 partial tiles are summed through distributed shared
+// memory (each rank reduces 128/KS columns and writes them to C), so split-K needs no
+// workspace, no zeroing pass and no atomics.  Instruction descriptor: A operand (B tile)
+// signed, B operand (A slice) unsigned; s32 accumulation mod 2^32.
+// ---------------------------------------------------------------------------------------------
+namespace tcs {
+constexpr int BN_ROWS = 128;  // rows of B per CTA (UMMA M)
+constexpr int MPAD = 16;      // A rows (UMMA N)
+constexpr int BK = 128;
+constexpr int THREADS = 256;
+template <int STAGES>
+struct Smem {
+    static constexpr int B_BYTES = BN_ROWS * BK;  // 16 KB
+    static constexpr int A_BYTES = MPAD * BK;     // 2 KB
+    static constexpr int STAGE_BYTES = B_BYTES + A_BYTES;
+    static constexpr int P_OFFSET = STAGES * STAGE_BYTES;
+    static constexpr int P_BYTES = MPAD * BN_ROWS * 4;  // partial tile [16 m][128 n] int32
+    static constexpr int BAR_OFFSET = P_OFFSET + P_BYTES;
+    static constexpr int TOTAL = BAR_OFFSET + (2 * STAGES + 2) * 8 + 16 + 1024;
+};
+}  // namespace tcs
+
+template <int STAGES>
+__global__ void __launch_bounds__(tcs::THREADS, 1)
+    tc_skinny_kernel(const __grid_constant__ CUtensorMap tma_b, const __grid_constant__ CUtensorMap tma_a,
+                     int32_t* __restrict__ C, int64_t ldc, int M, int N, int num_kb, int kb_per_cta) {
+    using S = tcs::Smem<STAGES>;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem + S::BAR_OFFSET);
+    uint64_t* empty = full + STAGES;
+    uint64_t* done = empty + STAGES;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 2);
+    int32_t* part = reinterpret_cast<int32_t*>(smem + S::P_OFFSET);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nt = blockIdx.x;
+    const int ks = blockIdx.y, nks = gridDim.y;  // cluster = the nks CTAs of this row tile
+    const int kb0 = ks * kb_per_cta, kb1 = min(num_kb, kb0 + kb_per_cta);
+
+    pdl_launch_dependents();
+    // The producer initialises the barriers and issues the first STAGES loads BEFORE the
+    // block-wide sync, so the DRAM latency overlaps TMEM allocation and the sync itself.
+    const uint64_t pol_b = policy_evict_first();  // B is streamed exactly once
+    const uint64_t pol_a = policy_evict_last();   // A is re-read by every CTA
+    int p_s = 0, p_kb = kb0;
+    uint32_t p_ph = 0;
+    if (warp == 0 && lane == 0) {
+        tma_prefetch(&tma_b);
+        tma_prefetch(&tma_a);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        mbar_init(&done[0], 1);
+        fence_mbar_init();
+        pdl_wait();  // inputs may come from the preceding kernel
+        for (; p_kb < kb1 && p_kb < kb0 + STAGES; ++p_kb) {
+            mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
+            uint8_t* sb = smem + p_s * S::STAGE_BYTES;
+            tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tcs::BK, nt * tcs::BN_ROWS, pol_b);
+            tma_load_2d(sb + S::B_BYTES, &tma_a, &full[p_s], p_kb * tcs::BK, 0, pol_a);
+            if (++p_s == STAGES) { p_s = 0; p_ph ^= 1; }
+        }
+    }
+    if (warp == 2) tmem_alloc<1>(tmem_slot, 32);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    pdl_wait();
+
+    if (warp == 0 && lane == 0) {
+        for (; p_kb < kb1; ++p_kb) {
+            mbar_wait(&empty[p_s], p_ph ^ 1);
+            mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
+            uint8_t* sb = smem + p_s * S::STAGE_BYTES;
+            tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tcs::BK, nt * tcs::BN_ROWS, pol_b);
+            tma_load_2d(sb + S::B_BYTES, &tma_a, &full[p_s], p_kb * tcs::BK, 0, pol_a);
+            if (++p_s == STAGES) { p_s = 0; p_ph ^= 1; }
+        }
+    } else if (warp == 1 && lane == 0) {
+        constexpr uint32_t idesc = idesc_i8(tcs::BN_ROWS, tcs::MPAD, /*a_signed=*/true, /*b_signed=*/false);
+        int s = 0;
+        uint32_t ph = 0;
+        for (int kb = kb0; kb < kb1; ++kb) {
+            mbar_wait(&full[s], ph);
+            tc_fence_after();
+            const uint32_t sb = smem_u32(smem + s * S::STAGE_BYTES);
+#pragma unroll
+            for (int k = 0; k < tcs::BK / 32; ++k)
+                mma_i8<1>(tmem_base, sdesc_k_sw128(sb + k * 32), sdesc_k_sw128(sb + S::B_BYTES + k * 32), idesc,
+                          (kb > kb0 || k > 0) ? 1u : 0u);
+            mma_commit(&empty[s]);
+            if (++s == STAGES) { s = 0; ph ^= 1; }
+        }
+        mma_commit(&done[0]);
+    } else if (warp >= 4) {
+        // partial tile TMEM -> smem [m][n]
+        const int ew = warp & 3;
+        const int nl = ew * 32 + lane;
+        if (kb0 < kb1) {
+            mbar_wait(&done[0], 0);
+            tc_fence_after();
+            uint32_t v[16];
+            tmem_ld_32x32b_x16(tmem_base + (static_cast<uint32_t>(ew * 32) << 16), v);
+            tmem_wait_ld();
+#pragma unroll
+            for (int m = 0; m < tcs::MPAD; ++m) part[m * tcs::BN_ROWS + nl] = static_cast<int32_t>(v[m]);
+        } else {
+#pragma unroll
+            for (int m = 0; m < tcs::MPAD; ++m) part[m * tcs::BN_ROWS + nl] = 0;
+        }
+    }
+    tc_fence_before();
+    if (nks > 1) cluster_sync(); else __syncthreads();
+
+    // rank ks reduces columns [ks*cw, (ks+1)*cw) of the tile over the cluster and writes C
+    const int cw = tcs::BN_ROWS / nks;  // host keeps nks a power of two <= 8
+    const uint32_t part_addr = smem_u32(part);
+    for (int i = threadIdx.x; i < tcs::MPAD * cw; i += tcs::THREADS) {
+        const int m = i / cw, nl = ks * cw + (i - m * cw);
+        const int n = nt * tcs::BN_ROWS + nl;
+        if (m >= M || n >= N) continue;
+        const uint32_t off = part_addr + static_cast<uint32_t>((m * tcs::BN_ROWS + nl) * 4);
+        uint32_t sum = static_cast<uint32_t>(part[m * tcs::BN_ROWS + nl]);
+        if (nks > 1) {
+            // issue all remote loads back to back, then add (latency overlaps)
+            uint32_t r[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) r[q] = (q < nks && q != ks) ? dsmem_ld_u32(off, q) : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sum += r[q];
+        }
+        C[static_cast<int64_t>(m) * ldc + n] = static_cast<int32_t>(sum);
+    }
+    if (nks > 1) cluster_sync(); else __syncthreads();  // peers may still read our partial
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<1>(tmem_base, 32);
     }
 }
 

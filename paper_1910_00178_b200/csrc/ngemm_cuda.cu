@@ -16,6 +16,7 @@
 #include <mutex>
 #include <string>
 #include <thread>
+#include <utility>
 #include <vector>
 
 #include "kernel_layout.cuh"
@@ -154,6 +155,52 @@ ngemm_status validate(const void* a, int64_t lda, const void* b, int64_t ldb, co
 }
 
 // ---------------------------------------------------------------- launchers
+// Programmatic dependent launch: consecutive kernels on a stream overlap the next kernel's
+// launch and prologue (barrier init, TMEM alloc, descriptor prefetch) with the tail of the
+// previous one; every kernel calls griddepcontrol.wait before touching global memory, so
+// stream order semantics are unchanged.  NGEMM_PDL=0 disables it.
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NGEMM_PDL");
+        return !(e && e[0] == '0');
+    }();
+    return on;
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, unsigned cx,
+                     unsigned cy, Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    unsigned na = 0;
+    if (cx * cy > 1) {
+        attr[na].id = cudaLaunchAttributeClusterDimension;
+        attr[na].val.clusterDim.x = cx;
+        attr[na].val.clusterDim.y = cy;
+        attr[na].val.clusterDim.z = 1;
+        ++na;
+    }
+    if (pdl_enabled()) {
+        attr[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        attr[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
+#define NG_LAUNCH(...)                                                                             \
+    do {                                                                                           \
+        cudaError_t e_ = launch_k(__VA_ARGS__);                                                    \
+        if (e_ != cudaSuccess) return fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e_)); \
+        g_launches.fetch_add(1, std::memory_order_relaxed);                                        \
+    } while (0)
+
 template <typename K>
 ngemm_status set_smem(K kernel, int bytes) {
     NG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
@@ -168,10 +215,11 @@ ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t
     dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
     if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
     if (mode == NGEMM_SAT_EXACT)
-        simt_gemm_kernel<1><<<grid, simt::THREADS, 0, st>>>(a, lda, b, ldb, c, ldc, m, n, k, vec_ok, c_vec);
+        NG_LAUNCH(simt_gemm_kernel<1>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, k, vec_ok,
+                  c_vec);
     else
-        simt_gemm_kernel<0><<<grid, simt::THREADS, 0, st>>>(a, lda, b, ldb, c, ldc, m, n, k, vec_ok, c_vec);
-    NG_LAUNCHED();
+        NG_LAUNCH(simt_gemm_kernel<0>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, k, vec_ok,
+                  c_vec);
     return NGEMM_OK;
 }
 
@@ -186,8 +234,8 @@ ngemm_status launch_simt_i16(const int16_t* a, int64_t lda, const int16_t* b, in
     const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
     dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
     if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
-    simt_gemm_kernel<2><<<grid, simt::THREADS, 0, st>>>(ab, lda * 2, bb, ldb * 2, c, ldc, m, n, k * 2, vec_ok, c_vec);
-    NG_LAUNCHED();
+    NG_LAUNCH(simt_gemm_kernel<2>, grid, dim3(simt::THREADS), 0, st, 1, 1, ab, lda * 2, bb, ldb * 2, c, ldc, m, n,
+              k * 2, vec_ok, c_vec);
     return NGEMM_OK;
 }
 
@@ -214,9 +262,8 @@ ngemm_status launch_skinny_t(const uint8_t* a, int64_t lda, const int8_t* b, int
     const int64_t groups = (n + NR - 1) / NR;
     int64_t blocks = (groups + skinny::WARPS - 1) / skinny::WARPS;
     blocks = std::min<int64_t>(blocks, static_cast<int64_t>(di.sms) * 8);
-    kern<<<static_cast<unsigned>(blocks), skinny::THREADS, smem, st>>>(a, lda, b, ldb, c, ldc, static_cast<int>(m), n,
-                                                                      k, kpad, b_vec);
-    NG_LAUNCHED();
+    NG_LAUNCH(kern, dim3(static_cast<unsigned>(blocks)), dim3(skinny::THREADS), smem, st, 1, 1, a, lda, b, ldb, c, ldc,
+              static_cast<int>(m), n, k, kpad, b_vec);
     return NGEMM_OK;
 }
 
@@ -230,11 +277,126 @@ ngemm_status launch_skinny_mode(const uint8_t* a, int64_t lda, const int8_t* b, 
     return launch_skinny_t<MODE, 16, 4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
 }
 
+// Makes (a, lda) and (b, ldb) TMA-describable: ragged operands are copied into a zero-padded
+// scratch buffer with 16-byte row pitch (SURVEY.md §0 gotcha 3).  Caller frees *scratch.
+ngemm_status stage_tma_operands(const uint8_t*& a, int64_t& lda, int64_t m, const uint8_t*& b, int64_t& ldb,
+                                int64_t n, int64_t k, uint8_t** scratch, cudaStream_t st) {
+    *scratch = nullptr;
+    const bool a_ok = tma_ok(a, lda), b_ok = tma_ok(b, ldb);
+    if (a_ok && b_ok) return NGEMM_OK;
+    const int64_t kp = round_up(k, 16);
+    const size_t bytes = static_cast<size_t>((a_ok ? 0 : m * kp) + (b_ok ? 0 : n * kp));
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(scratch), bytes, st));
+    uint8_t* p = *scratch;
+    if (!a_ok) {
+        NG_CUDA(cudaMemcpy2DAsync(p, kp, a, lda, k, m, cudaMemcpyDeviceToDevice, st));
+        a = p;
+        lda = kp;
+        p += m * kp;
+    }
+    if (!b_ok) {
+        NG_CUDA(cudaMemcpy2DAsync(p, kp, b, ldb, k, n, cudaMemcpyDeviceToDevice, st));
+        b = p;
+        ldb = kp;
+    }
+    return NGEMM_OK;
+}
+
+// Exact-mode skinny GEMM on the tensor cores (operands swapped, UMMA 128 x 16): 128-row tiles
+// of B x a K-split cluster of up to 8 CTAs reduced through DSMEM.
+ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                              int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    if (m > tcs::MPAD) return fail(NGEMM_ERR_UNSUPPORTED, "tensor-core skinny path needs M <= 16");
+    constexpr int STAGES = 4;
+    using S = tcs::Smem<STAGES>;
+    auto kern = tc_skinny_kernel<STAGES>;
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ngemm_status s = NGEMM_OK;
+    std::call_once(once[dev & 63], [&] { s = set_smem(kern, S::TOTAL); });
+    if (s != NGEMM_OK) return s;
+    const uint8_t* a_use = a;
+    const uint8_t* b_use = reinterpret_cast<const uint8_t*>(b);
+    int64_t lda_use = lda, ldb_use = ldb;
+    uint8_t* scratch = nullptr;
+    s = stage_tma_operands(a_use, lda_use, m, b_use, ldb_use, n, k, &scratch, st);
+    if (s != NGEMM_OK) return s;
+    const int n_tiles = static_cast<int>((n + tcs::BN_ROWS - 1) / tcs::BN_ROWS);
+    const int num_kb = static_cast<int>((k + tcs::BK - 1) / tcs::BK);
+    // cluster size along K: a power of two <= 8 (so 128 divides evenly), enough CTAs for ~2 waves
+    // about one CTA per SM, each streaming several K blocks (measured best on the c2 shapes)
+    int want = std::max(1, (di.sms + n_tiles - 1) / n_tiles);
+    if (const char* f = std::getenv("NGEMM_SKINNY_SPLITS")) want = std::max(1, std::atoi(f));
+    int ks = 1;
+    while (ks * 2 <= std::min(8, std::min(want, num_kb))) ks *= 2;
+    const int kb_per = (num_kb + ks - 1) / ks;
+    CUtensorMap tb, ta;
+    s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tcs::BK, tcs::BN_ROWS);
+    if (s == NGEMM_OK) s = make_tmap_u8(&ta, a_use, k, m, lda_use, tcs::BK, tcs::MPAD);
+    if (s == NGEMM_OK) {
+        cudaError_t e = launch_k(kern, dim3(n_tiles, ks), dim3(tcs::THREADS), S::TOTAL, st, 1, ks, tb, ta, c, ldc,
+                                 static_cast<int>(m), static_cast<int>(n), num_kb, kb_per);
+        if (e != cudaSuccess) s = fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+        else g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (scratch) cudaFreeAsync(scratch, st);
+    return s;
+}
+
+// Lanes-own-rows variant (skinny_rows_kernel): 32-row tiles of B x K splits.
+template <int MODE, int MT>
+ngemm_status launch_skinny_rows_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                  int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    const int64_t row_tiles = (n + 31) / 32;
+    const int64_t max_splits = std::max<int64_t>(1, (k + 255) / 256);
+    int64_t splits = std::min<int64_t>(max_splits, std::max<int64_t>(1, (2 * di.sms + row_tiles - 1) / row_tiles));
+    int64_t k_range = round_up((k + splits - 1) / splits, 256);
+    splits = (k + k_range - 1) / k_range;
+    const int smem = static_cast<int>(std::max<int64_t>(MT * k_range, 8 * MT * 32 * 4));
+    auto kern = skinny_rows_kernel<MODE, MT>;
+    if (smem > 48 * 1024) {
+        ngemm_status s = set_smem(kern, smem);
+        if (s != NGEMM_OK) return s;
+    }
+    if (splits > 1) {
+        if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
+        else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
+    }
+    const int b_vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0);
+    dim3 grid(static_cast<unsigned>(row_tiles), static_cast<unsigned>(splits));
+    NG_LAUNCH(kern, grid, dim3(skinny_rows::THREADS), smem, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k,
+              k_range, b_vec, splits > 1 ? 1 : 0);
+    return NGEMM_OK;
+}
+
+template <int MODE>
+ngemm_status launch_skinny_rows_mode(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                     int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di,
+                                     cudaStream_t st) {
+    if (m <= 1) return launch_skinny_rows_t<MODE, 1>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m <= 2) return launch_skinny_rows_t<MODE, 2>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m <= 4) return launch_skinny_rows_t<MODE, 4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m <= 8) return launch_skinny_rows_t<MODE, 8>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    return launch_skinny_rows_t<MODE, 16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+}
+
 ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                            int64_t m, int64_t n, int64_t k, int mode, const DevInfo& di, cudaStream_t st) {
-    if (!skinny_fits(m, k)) return fail(NGEMM_ERR_UNSUPPORTED, "skinny path needs M <= 16 and A resident in smem");
-    return mode == NGEMM_SAT_EXACT ? launch_skinny_mode<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
-                                   : launch_skinny_mode<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (m > kSkinnyMaxM) return fail(NGEMM_ERR_UNSUPPORTED, "skinny path needs M <= 16");
+    // Measured on B200 (profiles/sweep_skinny*.log): exact -> tensor-core swap-AB (2) on every
+    // c2 shape; saturating -> lanes-own-rows broadcast dp4a (1), except M = 1 with short K
+    // where the warp-butterfly variant (0) has the shorter latency chain.
+    int variant = mode == NGEMM_SAT_EXACT ? 2 : ((m == 1 && k <= 1024) ? 0 : 1);
+    if (const char* v = std::getenv("NGEMM_SKINNY_VARIANT")) variant = std::atoi(v);  // experiments
+    if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (variant == 0) {
+        if (!skinny_fits(m, k)) return fail(NGEMM_ERR_UNSUPPORTED, "skinny butterfly variant needs A resident in smem");
+        return mode == NGEMM_SAT_EXACT ? launch_skinny_mode<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
+                                       : launch_skinny_mode<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    }
+    return mode == NGEMM_SAT_EXACT ? launch_skinny_rows_mode<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
+                                   : launch_skinny_rows_mode<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
 }
 
 // 2-D int32 C [rows x cols] with row stride ldc elements, 32 x 32 boxes, SWIZZLE_128B (the
@@ -327,21 +489,8 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
     }
     const int grid = std::min(tiles * map.splits, units) * CG;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(grid);
-    cfg.blockDim = dim3(tc::THREADS);
-    cfg.dynamicSmemBytes = S::TOTAL;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CG;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    NG_CUDA(cudaLaunchKernelEx(&cfg, kern, ta, tb, tcmap, c, ldc, static_cast<int>(m), static_cast<int>(n), num_kb,
-                               map, c_mode));
-    NG_LAUNCHED();
+    NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
+              static_cast<int>(n), num_kb, map, c_mode);
     return NGEMM_OK;
 }
 
@@ -399,7 +548,8 @@ cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int
 
 int pick(int64_t m, int64_t n, int64_t k, int mode) {
     (void)n;
-    if (m <= kSkinnyMaxM && skinny_fits(m, k)) return NGEMM_KERNEL_SKINNY;
+    (void)k;
+    if (m <= kSkinnyMaxM) return NGEMM_KERNEL_SKINNY;
     if (mode == NGEMM_SAT_EXACT) return NGEMM_KERNEL_TCGEN05;
     return NGEMM_KERNEL_SIMT;
 }
@@ -469,9 +619,8 @@ ngemm_status repack_on(const ngemm_packed_meta* meta, const uint8_t* d_packed, u
     const int64_t kwords = (meta->k_orig + meta->h - 1) / meta->h;
     const int64_t total = meta->m_orig * kwords;
     const int64_t blocks = std::min<int64_t>((total + 255) / 256, 148 * 32);
-    repack_kernel<<<static_cast<unsigned>(blocks), 256, 0, st>>>(geom_of(meta), d_packed, d_a, lda * esize, kwords,
-                                                                 esize);
-    NG_LAUNCHED();
+    NG_LAUNCH(repack_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, geom_of(meta), d_packed, d_a,
+              lda * esize, kwords, esize);
     return NGEMM_OK;
 }
 

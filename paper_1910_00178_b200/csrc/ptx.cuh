@@ -151,7 +151,24 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
     return p;
 }
 
-// ---------------------------------------------------------------- cluster
+// ---------------------------------------------------------------- programmatic dependent launch
+// Wait until the preceding grid in the stream has completed and its memory is visible (no-op
+// when the kernel was not launched with programmatic stream serialization).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Let the dependent grid start launching (its CTAs run their prologue, then pdl_wait()).
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---------------------------------------------------------------- cluster / DSMEM
+__device__ __forceinline__ uint32_t dsmem_ld_u32(uint32_t local_smem_addr, uint32_t cta) {
+    uint32_t v;
+    asm volatile(
+        "{\n\t.reg .b32 ra;\n\t"
+        "mapa.shared::cluster.u32 ra, %1, %2;\n\t"
+        "ld.shared::cluster.u32 %0, [ra];\n\t}"
+        : "=r"(v)
+        : "r"(local_smem_addr), "r"(cta));
+    return v;
+}
 __device__ __forceinline__ uint32_t cluster_ctarank() {
     uint32_t r;
     asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));

@@ -295,3 +295,21 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
             b = oracle.mat_random_i8(n, k, n + cfg)
             got = dev_gemm(a, b, EXACT, "tcgen05", ldc=ldc)
             assert (got == oracle.gemm(a, b, EXACT)).all(), (cfg, splits, m, n, k, ldc)
+
+
+@pytest.mark.parametrize("variant", ["0", "1", "2"])
+def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
+    """Skinny (M <= 16) variants: 0 warp-butterfly dp4a, 1 lanes-own-rows dp4a (broadcast A),
+    2 tensor-core swap-AB (exact mode only; sat falls back to 1) — all bit-exact."""
+    monkeypatch.setenv("NGEMM_SKINNY_VARIANT", variant)
+    for c in golden["config2"]:
+        a = oracle.mat_random_u8(c["m"], c["k"], 0)
+        b = oracle.mat_normal_i8(c["n"], c["k"], 1, 32.0)
+        for mode, key in ((EXACT, "exact"), (SAT, "sat")):
+            assert oracle.fnv1a(dev_gemm(a, b, mode, "skinny")) == c[f"{key}_fnv"], (variant, c["m"], c["n"], c["k"])
+    for (m, n, k, lda, ldb, ldc) in ((3, 1000, 1000, 1000, 1000, 1000), (16, 129, 4097, 4112, 4100, 131),
+                                     (7, 70, 33, 40, 48, 70), (1, 5000, 160, 160, 160, 5003), (16, 300, 12288, None, None, None)):
+        a = oracle.mat_random_u8(m, k, m)
+        b = oracle.mat_random_i8(n, k, n)
+        for mode in (EXACT, SAT):
+            assert (dev_gemm(a, b, mode, "skinny", lda, ldb, ldc) == oracle.gemm(a, b, mode)).all(), (variant, m, n, k)
