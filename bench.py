@@ -170,23 +170,13 @@ def barrier(world):
 
 
 def max_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_1910_00178_b200 import dist as pdist
+    return pdist.reduce_max(x, world, device="cuda")
 
 
 def sum_over_ranks(x, world):
-    if world == 1:
-        return x
-    import torch
-    import torch.distributed as dist
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.SUM)
-    return float(t.item())
+    from paper_1910_00178_b200 import dist as pdist
+    return pdist.reduce_sum(x, world, device="cuda")
 
 
 def load_traffic(tag):
@@ -250,8 +240,8 @@ def run_ours(args):
     mode = EXACT if args.mode == "exact" else SAT
     kernel = {"auto": _lib.KERNEL_AUTO, "tcgen05": _lib.KERNEL_TCGEN05, "simt": _lib.KERNEL_SIMT,
               "skinny": _lib.KERNEL_SKINNY}[args.kernel]
-    rows = api.shard_rows(M, world, 128)
-    r0, r1 = rows[rank], rows[rank + 1]
+    from paper_1910_00178_b200 import dist as pdist
+    r0, r1 = pdist.row_block(M, rank, world, 128)
     mr = r1 - r0
     dev = torch.device("cuda", local)
 

@@ -46,10 +46,11 @@ template <int MODE>
 __global__ void __launch_bounds__(simt::THREADS, 2)
     simt_gemm_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                      int32_t* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int vec_ok,
-                     int c_vec_ok) {
+                     int c_vec_ok, const int32_t* __restrict__ guard) {
     using namespace simt;
     pdl_launch_dependents();
     pdl_wait();
+    if (guard != nullptr && sat_safe(guard)) return;  // the tensor-core kernel took this call
     __shared__ __align__(16) uint32_t As[BKW][LDS];
     __shared__ __align__(16) uint32_t Bs[BKW][LDS];
 

@@ -72,9 +72,14 @@ template <int BN, int STAGES, int CG>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
-                   int num_kb_total, TileMap map, int c_mode) {
+                   int num_kb_total, TileMap map, int c_mode, const int32_t* __restrict__ guard) {
     // c_mode: 0 = TMA tensor store of C (SWIZZLE_128B staging), 1 = TMA reduce-add into a
     // zeroed C (split-K), 2 = direct 128-byte row-segment stores (C not TMA-describable).
+    // guard: non-null for a HardwareSaturating call — run only if the operands cannot saturate.
+    if (guard != nullptr) {
+        pdl_wait();
+        if (!sat_safe(guard)) return;  // uniform across the grid (and across a CTA pair)
+    }
     using S = tc::Smem<BN, STAGES, CG>;
     constexpr int UMMA_M = tc::BM * CG;
     extern __shared__ uint8_t smem_raw[];

@@ -208,7 +208,7 @@ ngemm_status set_smem(K kernel, int bytes) {
 }
 
 ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
-                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st) {
+                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st, const int32_t* guard = nullptr) {
     const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
                         lda % 16 == 0 && ldb % 16 == 0);
     const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
@@ -216,10 +216,10 @@ ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t
     if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
     if (mode == NGEMM_SAT_EXACT)
         NG_LAUNCH(simt_gemm_kernel<1>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, k, vec_ok,
-                  c_vec);
+                  c_vec, guard);
     else
         NG_LAUNCH(simt_gemm_kernel<0>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, k, vec_ok,
-                  c_vec);
+                  c_vec, guard);
     return NGEMM_OK;
 }
 
@@ -235,7 +235,7 @@ ngemm_status launch_simt_i16(const int16_t* a, int64_t lda, const int16_t* b, in
     dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
     if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
     NG_LAUNCH(simt_gemm_kernel<2>, grid, dim3(simt::THREADS), 0, st, 1, 1, ab, lda * 2, bb, ldb * 2, c, ldc, m, n,
-              k * 2, vec_ok, c_vec);
+              k * 2, vec_ok, c_vec, static_cast<const int32_t*>(nullptr));
     return NGEMM_OK;
 }
 
@@ -464,7 +464,7 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
 template <int BN, int STAGES, int CG>
 ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcmap, int32_t* c,
                          int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int c_mode, const DevInfo& di,
-                         cudaStream_t st) {
+                         cudaStream_t st, const int32_t* guard) {
     using S = tc::Smem<BN, STAGES, CG>;
     auto kern = tc_gemm_kernel<BN, STAGES, CG>;
     static std::once_flag once[64];
@@ -490,12 +490,13 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     }
     const int grid = std::min(tiles * map.splits, units) * CG;
     NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
-              static_cast<int>(n), num_kb, map, c_mode);
+              static_cast<int>(n), num_kb, map, c_mode, guard);
     return NGEMM_OK;
 }
 
 ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
-                            int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+                            int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
+                            const int32_t* guard = nullptr) {
     // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3): stage ragged
     // operands through a zero-padded scratch copy (padding K at the end is neutral).
     const uint8_t* a_use = a;
@@ -530,10 +531,10 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
     const int c_mode = c_tma ? 0 : 2;
     if (s == NGEMM_OK) {
         switch (plan.cfg) {
-        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
-        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
-        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
-        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st); break;
+        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         }
     }
     if (scratch) cudaFreeAsync(scratch, st);
@@ -546,6 +547,34 @@ cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int
     return cudaMemcpy2DAsync(dst, kp, src, k, k, rows, cudaMemcpyHostToDevice, st);
 }
 
+// HardwareSaturating with a device-side proof: one pass computes the operand ranges; if no
+// int16 pair sum can leave [-32768, 32767] the exact tensor-core kernel runs (identical result),
+// otherwise the CUDA-core saturating kernel does — both are enqueued, each exits immediately
+// unless the proof selects it, so the stream never synchronises with the host.
+constexpr double kSatProofMinWork = 1 << 24;
+
+ngemm_status launch_sat_proved(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                               int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    int32_t* range = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&range), 16, st));
+    ngemm_status s = NGEMM_OK;
+    if (cudaMemsetAsync(range, 0, 16, st) != cudaSuccess) s = fail(NGEMM_ERR_CUDA, "memset(range) failed");
+    if (s == NGEMM_OK) {
+        const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
+                            lda % 16 == 0 && ldb % 16 == 0);
+        const int64_t chunks = (m + n) * ((k + 15) / 16);
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, di.sms * 8));
+        cudaError_t e = launch_k(operand_range_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, a,
+                                 lda, m, b, ldb, n, k, vec_ok, range);
+        if (e != cudaSuccess) s = fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+        else g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    if (s == NGEMM_OK) s = launch_tcgen05(a, lda, b, ldb, c, ldc, m, n, k, di, st, range);
+    if (s == NGEMM_OK) s = launch_simt(a, lda, b, ldb, c, ldc, m, n, k, NGEMM_SAT_HARDWARE, st, range);
+    cudaFreeAsync(range, st);
+    return s;
+}
+
 int pick(int64_t m, int64_t n, int64_t k, int mode) {
     (void)n;
     (void)k;
@@ -556,6 +585,7 @@ int pick(int64_t m, int64_t n, int64_t k, int mode) {
 
 ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc, int64_t m,
                       int64_t n, int64_t k, int mode, int kernel, cudaStream_t st) {
+    const bool auto_kernel = kernel == NGEMM_KERNEL_AUTO;
     ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, mode);
     if (s != NGEMM_OK) return s;
     int dev;
@@ -563,6 +593,9 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
     if (kernel == NGEMM_KERNEL_AUTO) kernel = pick(m, n, k, mode);
+    if (kernel == NGEMM_KERNEL_SIMT && mode == NGEMM_SAT_HARDWARE && auto_kernel && m > kSkinnyMaxM &&
+        static_cast<double>(m) * n * k >= kSatProofMinWork)
+        return launch_sat_proved(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     switch (kernel) {
     case NGEMM_KERNEL_SIMT: return launch_simt(a, lda, b, ldb, c, ldc, m, n, k, mode, st);
     case NGEMM_KERNEL_SKINNY: return launch_skinny(a, lda, b, ldb, c, ldc, m, n, k, mode, di, st);

@@ -158,6 +158,15 @@ __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;"
 // Let the dependent grid start launching (its CTAs run their prologue, then pdl_wait()).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// ---------------------------------------------------------------- saturation-safety guard
+// range = {max a (u8), max b, -min b} written by operand_range_kernel.  Every pair sum
+// a0*b0 + a1*b1 then lies in [-2*amax*bneg, 2*amax*bmax]; when that fits int16 the
+// HardwareSaturating result equals the exact one and the tensor cores may compute it.
+__device__ __forceinline__ int sat_safe(const int32_t* range) {
+    const int64_t amax = range[0], bmax = range[1], bneg = range[2];
+    return (2 * amax * bmax <= 32767 && 2 * amax * bneg <= 32768) ? 1 : 0;
+}
+
 // ---------------------------------------------------------------- cluster / DSMEM
 __device__ __forceinline__ uint32_t dsmem_ld_u32(uint32_t local_smem_addr, uint32_t cta) {
     uint32_t v;

@@ -313,3 +313,26 @@ def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
         b = oracle.mat_random_i8(n, k, n)
         for mode in (EXACT, SAT):
             assert (dev_gemm(a, b, mode, "skinny", lda, ldb, ldc) == oracle.gemm(a, b, mode)).all(), (variant, m, n, k)
+
+
+def test_sat_mode_on_provably_safe_inputs(cuda, oracle):
+    """HardwareSaturating on inputs that cannot saturate (the reference's safe range, u8 <= 127,
+    tuner.hpp:26-43): the device-side range proof routes the call to the tensor cores; the
+    result must still equal gemm_sat_oracle (== gemm_ref here).  Also the boundary cases."""
+    for (m, n, k) in ((512, 512, 1024), (1000, 700, 333), (2048, 2048, 2048)):
+        a = oracle.mat_random_u8(m, k, 3, 0, 127)
+        b = oracle.mat_random_i8(n, k, 4)
+        got = dev_gemm(a, b, SAT, "auto")
+        assert (got == oracle.gemm(a, b, SAT)).all() and (got == oracle.gemm(a, b, EXACT)).all()
+    # 2*amax*bmax = 2*128*127 = 32512 <= 32767 but 2*amax*bneg = 2*128*128 = 32768: still safe
+    a = np.full((300, 256), 128, np.uint8)
+    b = np.where(np.arange(200 * 256).reshape(200, 256) % 3 == 0, -128, 127).astype(np.int8)
+    assert (dev_gemm(a, b, SAT, "auto") == oracle.gemm(a, b, SAT)).all()
+    # one byte over the edge: 129 * 127 * 2 = 32766 ok, 129 * 128 * 2 = 33024 saturates
+    a[7, 10] = 129
+    a[7, 11] = 129
+    b[:, 10] = -128
+    b[:, 11] = -128
+    got = dev_gemm(a, b, SAT, "auto")
+    assert (got == oracle.gemm(a, b, SAT)).all()
+    assert (got != oracle.gemm(a, b, EXACT)).any()
