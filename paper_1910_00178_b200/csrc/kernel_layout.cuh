@@ -55,6 +55,22 @@ __global__ void repack_kernel(PackedGeom g, const uint8_t* __restrict__ packed, 
     }
 }
 
+// Zeroes C [m x n] (row stride ldc) for a split-K launch — but only when the saturation
+// guard selects the kernel that follows (want_safe = 1: the tensor-core kernel, 0: the
+// CUDA-core one), so the path that does not run never clobbers the other's result.
+__global__ void guarded_zero_kernel(int32_t* __restrict__ c, int64_t ldc, int64_t m, int64_t n,
+                                    const int32_t* __restrict__ guard, int want_safe) {
+    pdl_launch_dependents();
+    pdl_wait();
+    if (sat_safe(guard) != want_safe) return;
+    const int64_t total = m * n;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / n;
+        c[r * ldc + (i - r * n)] = 0;
+    }
+}
+
 // Operand ranges for the saturation-safety proof of the dispatcher: out = {max A, max B, -min B}
 // (out zeroed by the caller).  Rows are scanned in 16-byte chunks with packed-byte SIMD
 // (__vmaxu4 / __vmaxs4 / __vmins4) when aligned; one atomicMax per warp.

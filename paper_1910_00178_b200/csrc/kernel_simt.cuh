@@ -10,9 +10,12 @@
 // last element with 0 (gemm.hpp:95-96).  All int32 adds wrap, so the summation order is
 // immaterial (common.hpp:129-135).
 //
-// Tiling: 128x128 output tile per 256-thread CTA, 8x8 outputs per thread, K staged through
-// shared memory 32 bytes (8 words) at a time, transposed to word-major so the inner loop is
-// two LDS.128 per operand; next-tile global loads are prefetched into registers.
+// Tiling: 128x128 (8x8 outputs per thread) or 64x64 (4x4) output tiles per 256-thread CTA,
+// K staged through shared memory 32 bytes (8 words) at a time, transposed to word-major so the
+// inner loop is LDS.128 per 4 operand words; next-stage global loads are prefetched into
+// registers.  Small problems add K splits (atomic wrap-add into a zeroed C) to fill 148 SMs.
+// The saturating inner step is 2 IDP.4A + 4 VIMNMX + 1 IADD3 per 4 MACs — CUDA-core (ALU
+// pipe) bound, which is why inputs that provably cannot saturate go to the tensor cores.
 #pragma once
 
 #include "ptx.cuh"
@@ -20,8 +23,7 @@
 namespace ngemm_dev {
 
 namespace simt {
-constexpr int BM = 128, BN = 128, BKW = 8;  // BK = 32 bytes
-constexpr int LDS = BM + 4;                  // padded word stride (bank-conflict free stores)
+constexpr int BKW = 8;  // BK = 32 bytes (8 K-words) per smem stage
 constexpr int THREADS = 256;
 }  // namespace simt
 
@@ -42,12 +44,18 @@ __device__ __forceinline__ uint4 simt_load16(const uint8_t* __restrict__ base, i
 // MODE: 1 = WideningExact, 0 = HardwareSaturating (u8 x s8 words of 4 K-elements);
 //       2 = the 16-bit path, i16 x i16 words of 2 K-elements (madd_pair_i16, lanes.hpp:42-47:
 //           no saturation stage, everything mod 2^32).  K, lda, ldb are in BYTES here.
-template <int MODE>
+// TILE: 128 (8x8 outputs per thread) or 64 (4x4, for small shapes).  blockIdx.z selects a
+// K split of k_split bytes (a multiple of 32, so pairs stay even-aligned); with split > 1
+// the partials are wrap-added into a zeroed C.
+template <int MODE, int TILE>
 __global__ void __launch_bounds__(simt::THREADS, 2)
     simt_gemm_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                      int32_t* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int vec_ok,
-                     int c_vec_ok, const int32_t* __restrict__ guard) {
+                     int c_vec_ok, const int32_t* __restrict__ guard, int64_t k_split, int accumulate) {
     using namespace simt;
+    constexpr int TT = TILE / 16;     // outputs per thread per dimension
+    constexpr int LDS = TILE + 4;     // padded word stride (bank-conflict free stores)
+    constexpr int LOADS = (TILE * 2 + THREADS - 1) / THREADS;  // uint4 loads per operand per thread
     pdl_launch_dependents();
     pdl_wait();
     if (guard != nullptr && sat_safe(guard)) return;  // the tensor-core kernel took this call
@@ -56,61 +64,76 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
 
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
-    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * BM;
-    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * BN;
+    const int64_t m0 = static_cast<int64_t>(blockIdx.y) * TILE;
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * TILE;
+    const int64_t kb = static_cast<int64_t>(blockIdx.z) * k_split;
+    const int64_t ke = min(K, kb + k_split);
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
 
-    // loader mapping: row lr, 16-byte half lh of the 32-byte K slice
-    const int lr = tid >> 1, lh = tid & 1;
-
-    int32_t acc[8][8];
+    int32_t acc[TT][TT];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < TT; ++i)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) acc[i][j] = 0;
+        for (int j = 0; j < TT; ++j) acc[i][j] = 0;
 
-    const int64_t nk = (K + 31) / 32;
-    uint4 ra = simt_load16(A, lda, m0 + lr, M, lh * 16, K, vec_ok);
-    uint4 rb = simt_load16(Bu, ldb, n0 + lr, N, lh * 16, K, vec_ok);
+    const int64_t nk = (ke - kb + 31) / 32;
+    uint4 ra[LOADS], rb[LOADS];
+#pragma unroll
+    for (int l = 0; l < LOADS; ++l) {
+        const int li = tid + l * THREADS, lr = li >> 1, lh = li & 1;
+        ra[l] = li < TILE * 2 ? simt_load16(A, lda, m0 + lr, M, kb + lh * 16, ke, vec_ok) : make_uint4(0, 0, 0, 0);
+        rb[l] = li < TILE * 2 ? simt_load16(Bu, ldb, n0 + lr, N, kb + lh * 16, ke, vec_ok) : make_uint4(0, 0, 0, 0);
+    }
 
     for (int64_t kt = 0; kt < nk; ++kt) {
         __syncthreads();
-        As[lh * 4 + 0][lr] = ra.x;
-        As[lh * 4 + 1][lr] = ra.y;
-        As[lh * 4 + 2][lr] = ra.z;
-        As[lh * 4 + 3][lr] = ra.w;
-        Bs[lh * 4 + 0][lr] = rb.x;
-        Bs[lh * 4 + 1][lr] = rb.y;
-        Bs[lh * 4 + 2][lr] = rb.z;
-        Bs[lh * 4 + 3][lr] = rb.w;
+#pragma unroll
+        for (int l = 0; l < LOADS; ++l) {
+            const int li = tid + l * THREADS, lr = li >> 1, lh = li & 1;
+            if (li < TILE * 2) {
+                As[lh * 4 + 0][lr] = ra[l].x;
+                As[lh * 4 + 1][lr] = ra[l].y;
+                As[lh * 4 + 2][lr] = ra[l].z;
+                As[lh * 4 + 3][lr] = ra[l].w;
+                Bs[lh * 4 + 0][lr] = rb[l].x;
+                Bs[lh * 4 + 1][lr] = rb[l].y;
+                Bs[lh * 4 + 2][lr] = rb[l].z;
+                Bs[lh * 4 + 3][lr] = rb[l].w;
+            }
+        }
         __syncthreads();
         if (kt + 1 < nk) {
-            const int64_t kn = (kt + 1) * 32 + lh * 16;
-            ra = simt_load16(A, lda, m0 + lr, M, kn, K, vec_ok);
-            rb = simt_load16(Bu, ldb, n0 + lr, N, kn, K, vec_ok);
+#pragma unroll
+            for (int l = 0; l < LOADS; ++l) {
+                const int li = tid + l * THREADS, lr = li >> 1, lh = li & 1;
+                if (li < TILE * 2) {
+                    const int64_t kn = kb + (kt + 1) * 32 + lh * 16;
+                    ra[l] = simt_load16(A, lda, m0 + lr, M, kn, ke, vec_ok);
+                    rb[l] = simt_load16(Bu, ldb, n0 + lr, N, kn, ke, vec_ok);
+                }
+            }
         }
 #pragma unroll
         for (int kw = 0; kw < BKW; ++kw) {
-            uint32_t a[8], b[8];
-            const uint4 a0 = *reinterpret_cast<const uint4*>(&As[kw][ty * 4]);
-            const uint4 a1 = *reinterpret_cast<const uint4*>(&As[kw][64 + ty * 4]);
-            const uint4 b0 = *reinterpret_cast<const uint4*>(&Bs[kw][tx * 4]);
-            const uint4 b1 = *reinterpret_cast<const uint4*>(&Bs[kw][64 + tx * 4]);
-            a[0] = a0.x; a[1] = a0.y; a[2] = a0.z; a[3] = a0.w;
-            a[4] = a1.x; a[5] = a1.y; a[6] = a1.z; a[7] = a1.w;
-            b[0] = b0.x; b[1] = b0.y; b[2] = b0.z; b[3] = b0.w;
-            b[4] = b1.x; b[5] = b1.y; b[6] = b1.z; b[7] = b1.w;
+            uint32_t a[TT], b[TT];
+#pragma unroll
+            for (int h = 0; h < TT / 4; ++h) {
+                const uint4 av = *reinterpret_cast<const uint4*>(&As[kw][h * (TILE / 2) + ty * 4]);
+                const uint4 bv = *reinterpret_cast<const uint4*>(&Bs[kw][h * (TILE / 2) + tx * 4]);
+                a[h * 4 + 0] = av.x; a[h * 4 + 1] = av.y; a[h * 4 + 2] = av.z; a[h * 4 + 3] = av.w;
+                b[h * 4 + 0] = bv.x; b[h * 4 + 1] = bv.y; b[h * 4 + 2] = bv.z; b[h * 4 + 3] = bv.w;
+            }
             if constexpr (MODE == 1) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i)
+                for (int i = 0; i < TT; ++i)
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) acc[i][j] = dp4a_us(a[i], b[j], acc[i][j]);
+                    for (int j = 0; j < TT; ++j) acc[i][j] = dp4a_us(a[i], b[j], acc[i][j]);
             } else if constexpr (MODE == 2) {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < TT; ++i) {
                     const int32_t alo = static_cast<int16_t>(a[i] & 0xFFFFu), ahi = static_cast<int32_t>(a[i]) >> 16;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < TT; ++j) {
                         const int32_t blo = static_cast<int16_t>(b[j] & 0xFFFFu), bhi = static_cast<int32_t>(b[j]) >> 16;
                         acc[i][j] = static_cast<int32_t>(static_cast<uint32_t>(acc[i][j]) +
                                                          static_cast<uint32_t>(alo * blo) +
@@ -119,10 +142,10 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
                 }
             } else {
 #pragma unroll
-                for (int i = 0; i < 8; ++i) {
+                for (int i = 0; i < TT; ++i) {
                     const uint32_t alo = a[i] & 0x0000FFFFu, ahi = a[i] & 0xFFFF0000u;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
+                    for (int j = 0; j < TT; ++j) {
                         const int32_t p0 = clamp_i16(dp4a_us(alo, b[j], 0));
                         const int32_t p1 = clamp_i16(dp4a_us(ahi, b[j], 0));
                         acc[i][j] = static_cast<int32_t>(static_cast<uint32_t>(acc[i][j]) +
@@ -134,14 +157,19 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
     }
 
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-        const int64_t row = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    for (int i = 0; i < TT; ++i) {
+        const int64_t row = m0 + (i / 4) * (TILE / 2) + ty * 4 + (i % 4);
         if (row >= M) continue;
         int32_t* crow = C + row * ldc;
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int64_t col = n0 + h * 64 + tx * 4;
-            if (c_vec_ok && col + 4 <= N) {
+        for (int h = 0; h < TT / 4; ++h) {
+            const int64_t col = n0 + h * (TILE / 2) + tx * 4;
+            if (accumulate) {
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (col + j < N) atomicAdd(reinterpret_cast<unsigned int*>(crow + col + j),
+                                               static_cast<unsigned int>(acc[i][h * 4 + j]));
+            } else if (c_vec_ok && col + 4 <= N) {
                 *reinterpret_cast<int4*>(crow + col) =
                     make_int4(acc[i][h * 4 + 0], acc[i][h * 4 + 1], acc[i][h * 4 + 2], acc[i][h * 4 + 3]);
             } else {

@@ -207,36 +207,70 @@ ngemm_status set_smem(K kernel, int bytes) {
     return NGEMM_OK;
 }
 
-ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
-                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st, const int32_t* guard = nullptr) {
+// Zero C before a split-K launch: a plain memset, or — on the guarded saturating path — a
+// kernel that only zeroes when the guard selects the launch that follows.
+ngemm_status zero_c(int32_t* c, int64_t ldc, int64_t m, int64_t n, const int32_t* guard, int want_safe,
+                    const DevInfo& di, cudaStream_t st) {
+    if (guard == nullptr) {
+        if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
+        else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
+        return NGEMM_OK;
+    }
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((m * n + 255) / 256, di.sms * 4));
+    NG_LAUNCH(guarded_zero_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, c, ldc, m, n, guard,
+              want_safe);
+    return NGEMM_OK;
+}
+
+// CUDA-core kernel launch: 128x128 tiles when they fill two waves of CTAs, else 64x64 tiles
+// plus K splits (32-byte aligned) so that ~2 CTAs per SM are busy.  kbytes/lda/ldb in bytes.
+template <int MODE>
+ngemm_status launch_simt_bytes(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                               int64_t m, int64_t n, int64_t kbytes, const DevInfo& di, cudaStream_t st,
+                               const int32_t* guard) {
     const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
                         lda % 16 == 0 && ldb % 16 == 0);
     const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
-    dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
-    if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
-    if (mode == NGEMM_SAT_EXACT)
-        NG_LAUNCH(simt_gemm_kernel<1>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, k, vec_ok,
-                  c_vec, guard);
-    else
-        NG_LAUNCH(simt_gemm_kernel<0>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, k, vec_ok,
-                  c_vec, guard);
+    const int64_t tiles128 = ((m + 127) / 128) * ((n + 127) / 128);
+    const int64_t target = 2 * di.sms;
+    if (tiles128 >= target || (m + 63) / 64 > 65535) {
+        dim3 grid(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>((m + 127) / 128), 1);
+        if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
+        NG_LAUNCH(simt_gemm_kernel<MODE, 128>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n,
+                  kbytes, vec_ok, c_vec, guard, kbytes, 0);
+        return NGEMM_OK;
+    }
+    const int64_t tiles64 = ((m + 63) / 64) * ((n + 63) / 64);
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((target + tiles64 - 1) / tiles64, kbytes / 512));
+    const int64_t k_split = round_up((kbytes + splits - 1) / splits, 32);
+    splits = (kbytes + k_split - 1) / k_split;
+    if (splits > 1) {
+        ngemm_status zs = zero_c(c, ldc, m, n, guard, 0, di, st);
+        if (zs != NGEMM_OK) return zs;
+    }
+    dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64), static_cast<unsigned>(splits));
+    NG_LAUNCH(simt_gemm_kernel<MODE, 64>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, kbytes,
+              vec_ok, c_vec, guard, k_split, splits > 1 ? 1 : 0);
     return NGEMM_OK;
+}
+
+ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st, const int32_t* guard = nullptr) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const DevInfo di = dev_info(dev);
+    return mode == NGEMM_SAT_EXACT ? launch_simt_bytes<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st, guard)
+                                   : launch_simt_bytes<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st, guard);
 }
 
 // i16 x i16 -> i32 (the reference's 16-bit path, gemm.hpp:161-190, 245-281): SIMT kernel in
 // MODE 2 over the operands viewed as bytes (2 bytes per element, K-groups of 2 per word).
 ngemm_status launch_simt_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                              int64_t m, int64_t n, int64_t k, cudaStream_t st) {
-    const uint8_t* ab = reinterpret_cast<const uint8_t*>(a);
-    const int8_t* bb = reinterpret_cast<const int8_t*>(b);
-    const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
-                        (lda * 2) % 16 == 0 && (ldb * 2) % 16 == 0);
-    const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
-    dim3 grid(static_cast<unsigned>((n + simt::BN - 1) / simt::BN), static_cast<unsigned>((m + simt::BM - 1) / simt::BM));
-    if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
-    NG_LAUNCH(simt_gemm_kernel<2>, grid, dim3(simt::THREADS), 0, st, 1, 1, ab, lda * 2, bb, ldb * 2, c, ldc, m, n,
-              k * 2, vec_ok, c_vec, static_cast<const int32_t*>(nullptr));
-    return NGEMM_OK;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return launch_simt_bytes<2>(reinterpret_cast<const uint8_t*>(a), lda * 2, reinterpret_cast<const int8_t*>(b),
+                                ldb * 2, c, ldc, m, n, k * 2, dev_info(dev), st, nullptr);
 }
 
 constexpr int kSkinnyMaxM = 16;
@@ -485,8 +519,8 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
     if (map.splits > 1) {
         c_mode = 1;
-        if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
-        else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
+        ngemm_status zs = zero_c(c, ldc, m, n, guard, 1, di, st);
+        if (zs != NGEMM_OK) return zs;
     }
     const int grid = std::min(tiles * map.splits, units) * CG;
     NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
