@@ -408,11 +408,13 @@ def run_reference(args):
     # same distributions as our arm (host-side seeded draws; the reference has its own PRNG)
     rng = np.random.default_rng(0)
     threads = os.cpu_count() or 1
-    # bounded sample: enough rows for ~3 s per step on all host threads
+    # bounded sample: rows sized so each step takes ~min(3 s, 100 s / (steps + warmup)) on all
+    # host threads, keeping the whole reference run within a few minutes
+    step_s = min(3.0, 100.0 / max(1, args.steps + args.warmup))
     b = rng.integers(-128, 128, (N, K), dtype=np.int8)
     a_probe = rng.integers(0, 256, (min(M, threads), K), dtype=np.uint8)
     _, _, kind, _, dt = cpu_reference_sample(a_probe, b, N, K, mode, target_s=0.0)
-    rows = min(M, max(threads, int(threads * 3.0 / max(dt, 1e-3)) // threads * threads))
+    rows = min(M, max(threads, int(threads * step_s / max(dt, 1e-3)) // threads * threads))
     a = rng.integers(0, 256, (rows, K), dtype=np.uint8)
     variant = "gemm_ref" if mode == EXACT else "gemm_conventional"
     if Reference.available():

@@ -713,6 +713,73 @@ ngemm_status run_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ld
     return launch_simt_i16(a, lda, b, ldb, c, ldc, m, n, k, st);
 }
 
+bool is_pinned(const void* p) {
+    cudaPointerAttributes attr;
+    if (cudaPointerGetAttributes(&attr, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return attr.type == cudaMemoryTypeHost;
+}
+
+// Large GEMM on PINNED host buffers: A is streamed in row chunks on a copy-in stream, each
+// chunk's GEMM runs on a compute stream as soon as its rows (and B) have landed, and its C
+// rows go back on a copy-out stream — H2D, tensor-core compute and D2H overlap across chunks
+// (PCIe is full duplex), instead of copy-all / compute / copy-all.
+ngemm_status host_gemm_pipelined(const uint8_t* a, const int8_t* b, int32_t* c, int64_t m, int64_t n, int64_t k,
+                                 int sat_mode, int kernel) {
+    const int64_t kp = round_up(k, 16);
+    const int64_t chunk = round_up((m + 7) / 8, 256);
+    const int nchunks = static_cast<int>((m + chunk - 1) / chunk);
+    const size_t a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
+    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
+    const size_t b_off = round_up(static_cast<int64_t>(a_bytes), 256), c_off = b_off + round_up(b_bytes, 256);
+    cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * nchunks + 2), nullptr);
+    ngemm_status s = NGEMM_OK;
+    auto ck = [&](cudaError_t e, const char* what) {
+        if (e != cudaSuccess && s == NGEMM_OK) s = fail(NGEMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+        return s == NGEMM_OK;
+    };
+    ck(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking), "stream");
+    ck(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking), "stream");
+    for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    uint8_t* buf = nullptr;
+    if (s == NGEMM_OK && ck(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, sin), "malloc")) {
+        cudaEvent_t ev_b = ev[0], ev_done = ev[1];
+        ck(copy_rows_h2d(buf + b_off, kp, b, k, n, sin), "H2D B");
+        ck(cudaEventRecord(ev_b, sin), "record");
+        ck(cudaStreamWaitEvent(scomp, ev_b, 0), "wait");
+        for (int i = 0; i < nchunks && s == NGEMM_OK; ++i) {
+            const int64_t r0 = i * chunk, rows = std::min(chunk, m - r0);
+            cudaEvent_t ev_a = ev[2 + 2 * i], ev_c = ev[3 + 2 * i];
+            ck(copy_rows_h2d(buf + r0 * kp, kp, a + r0 * k, k, rows, sin), "H2D A");
+            ck(cudaEventRecord(ev_a, sin), "record");
+            ck(cudaStreamWaitEvent(scomp, ev_a, 0), "wait");
+            if (s == NGEMM_OK)
+                s = run_gemm(buf + r0 * kp, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
+                             reinterpret_cast<int32_t*>(buf + c_off) + r0 * n, n, rows, n, k, sat_mode, kernel, scomp);
+            ck(cudaEventRecord(ev_c, scomp), "record");
+            ck(cudaStreamWaitEvent(sout, ev_c, 0), "wait");
+            ck(cudaMemcpyAsync(c + r0 * n, buf + c_off + static_cast<size_t>(r0 * n) * 4,
+                               static_cast<size_t>(rows * n) * 4, cudaMemcpyDeviceToHost, sout), "D2H C");
+        }
+        ck(cudaEventRecord(ev_done, sout), "record");
+        cudaStreamWaitEvent(sin, ev_done, 0);
+        cudaFreeAsync(buf, sin);
+    }
+    if (sin) ck(cudaStreamSynchronize(sin), "sync");
+    if (sout) ck(cudaStreamSynchronize(sout), "sync");
+    if (scomp) ck(cudaStreamSynchronize(scomp), "sync");
+    for (auto& e : ev)
+        if (e) cudaEventDestroy(e);
+    if (sin) cudaStreamDestroy(sin);
+    if (scomp) cudaStreamDestroy(scomp);
+    if (sout) cudaStreamDestroy(sout);
+    return s;
+}
+
 // Host operands -> pooled device buffers (rows padded to 16 bytes for TMA) -> optional device
 // repack of a packed weight -> GEMM -> host C.  esize selects the u8 x i8 or i16 x i16 path.
 ngemm_status host_gemm(int esize, const ngemm_packed_meta* meta, const void* a_or_packed, size_t packed_bytes,
@@ -908,6 +975,13 @@ ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_
                                        int sat_mode, int kernel) {
     ngemm_status s = validate(a, k, b, k, c, n, m, n, k, sat_mode);
     if (s != NGEMM_OK) return s;
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    // big outputs on pinned host memory: overlap H2D / compute / D2H in row chunks
+    if (m >= 1024 && static_cast<double>(m) * n * 4 >= 64.0 * (1 << 20) && is_pinned(a) && is_pinned(c))
+        return host_gemm_pipelined(a, b, c, m, n, k, sat_mode, kernel);
     return host_gemm(1, nullptr, a, 0, b, c, m, n, k, sat_mode, kernel);
 }
 

@@ -336,3 +336,20 @@ def test_sat_mode_on_provably_safe_inputs(cuda, oracle):
     got = dev_gemm(a, b, SAT, "auto")
     assert (got == oracle.gemm(a, b, SAT)).all()
     assert (got != oracle.gemm(a, b, EXACT)).any()
+
+
+def test_host_entry_pipelined_pinned(cuda, oracle):
+    """ngemm_cuda_gemm_u8i8_host on PINNED host buffers takes the chunked H2D/compute/D2H
+    pipeline (C >= 64 MiB); result must equal the oracle in both modes."""
+    import torch
+    m, n, k = 4096, 4096, 640
+    a = oracle.mat_random_u8(m, k, 11)
+    b = oracle.mat_random_i8(n, k, 12)
+    ta = torch.from_numpy(a).pin_memory()
+    tb = torch.from_numpy(b).pin_memory()
+    tc = torch.empty((m, n), dtype=torch.int32).pin_memory()
+    L = _lib.load()
+    for mode in (EXACT, SAT):
+        tc.fill_(-1)
+        _lib.check(L.ngemm_cuda_gemm_u8i8_host(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), m, n, k, mode, 0))
+        assert (tc.numpy() == oracle.gemm(a, b, mode)).all(), mode
