@@ -64,6 +64,7 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
 
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
+    const int32_t one = (k_split > 0) ? 1 : 0;  // a runtime 1 the compiler cannot fold
     const int64_t m0 = static_cast<int64_t>(blockIdx.y) * TILE;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * TILE;
     const int64_t kb = static_cast<int64_t>(blockIdx.z) * k_split;
@@ -148,8 +149,9 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
                     for (int j = 0; j < TT; ++j) {
                         const int32_t p0 = clamp_i16(dp4a_us(alo, b[j], 0));
                         const int32_t p1 = clamp_i16(dp4a_us(ahi, b[j], 0));
-                        acc[i][j] = static_cast<int32_t>(static_cast<uint32_t>(acc[i][j]) +
-                                                         static_cast<uint32_t>(p0) + static_cast<uint32_t>(p1));
+                        // the two clamps already occupy the ALU pipe (VIMNMX); accumulate on the
+                        // FMA pipe (IMAD with a runtime 1) to balance the two pipes
+                        acc[i][j] = imad_u32(p0, one, imad_u32(p1, one, acc[i][j]));
                     }
                 }
             }

@@ -22,6 +22,13 @@ __device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
 
 __device__ __forceinline__ int32_t clamp_i16(int32_t x) { return max(-32768, min(32767, x)); }
 
+// a * b + c on the FMA pipe (IMAD), wrapping mod 2^32.
+__device__ __forceinline__ int32_t imad_u32(int32_t a, int32_t b, int32_t c) {
+    int32_t d;
+    asm("mad.lo.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
 __device__ __forceinline__ bool elect_one() {
     uint32_t pred = 0;
     asm volatile(
