@@ -259,3 +259,133 @@ __global__ void __launch_bounds__(skinny_rows::THREADS)
 }
 
 }  // namespace ngemm_dev
+
+namespace ngemm_dev {
+
+// ---------------------------------------------------------------------------------------------
+// skinny_mma_kernel — exact-mode skinny GEMM (M <= 16) as a pure load stream.  Each warp owns 16
+// rows of B and one K slice; every thread keeps 16-byte loads of B in flight and feeds warp-level
+// integer MMAs (mma.sync m16n8k32 u8 x s8 -> s32: B rows as the MMA's M, the <= 16 rows of A,
+// broadcast from shared memory, as its N).  No TMEM, TMA descriptors, mbarriers or clusters —
+// for a 0.6-4.5 MB operand the kernel's latency chain, not the math, is the cost (see
+// scripts/probes/floor.cu: a bare 4 MB load stream takes ~2 us).  Because the dot product is
+// order independent mod 2^32, the K bytes of a 128-byte chunk are assigned to MMA k-groups by
+// thread (t owns bytes [t*16, t*16+16) and [64 + t*16, 64 + t*16 + 16)) — the SAME mapping for
+// A and B — so every B load is a full 16-byte vector.  The CTA's warps split K and meet once in
+// shared memory; grid K splits (if any) wrap-add into a zeroed C.
+// ---------------------------------------------------------------------------------------------
+namespace skinny_mma {
+constexpr int CHUNK = 128;  // bytes of K per warp step
+}  // namespace skinny_mma
+
+__device__ __forceinline__ void mma_u8s8_m16n8k32(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
+                                                  uint32_t a3, uint32_t b0, uint32_t b1) {
+    // A operand (row-major 16x32) signed: B's rows; B operand (col-major 32x8) unsigned: A's rows.
+    asm volatile(
+        "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
+        : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
+        : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
+}
+
+// WARPS per CTA (8/16/32); RG: 16-row groups per CTA; KS = WARPS / RG warps split the CTA's
+// K range.  MT: 8 or 16.
+// A (<= 16 rows) is read straight through L1 (every warp of the CTA re-reads the same few KB),
+// so the kernel's first instructions are the B loads: no staging pass, no block barrier before
+// the stream starts.
+template <int MT, int RG, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    skinny_mma_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
+                      int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range,
+                      int vec_ok, int accumulate) {
+    constexpr int KS = WARPS / RG;
+    constexpr int NB = MT / 8;  // n8 blocks of A rows
+    __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    pdl_launch_dependents();
+    pdl_wait();
+    const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
+    const int64_t kend = min(K, kbeg + k_range);
+    const int rg = warp / KS, ks = warp % KS;
+    const int64_t n0 = (static_cast<int64_t>(blockIdx.x) * RG + rg) * 16;
+    const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
+
+    // 16 bytes of row `row` of X at byte k (zero outside rows/K); streaming or L1-cached
+    auto load16 = [&](const uint8_t* X, int64_t ld, int64_t rows, int64_t row, int64_t k, bool stream) -> uint4 {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row >= rows || k >= kend) return v;
+        const uint8_t* p = X + row * ld + k;
+        if (vec_ok && k + 16 <= kend) {
+            if (stream)
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+            else
+                v = __ldg(reinterpret_cast<const uint4*>(p));
+            return v;
+        }
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (k + i < kend) w[i >> 2] |= static_cast<uint32_t>(__ldg(p + i)) << (8 * (i & 3));
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    };
+
+    int32_t d[NB][4];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) d[j][0] = d[j][1] = d[j][2] = d[j][3] = 0;
+
+    const int64_t chunks = (kend - kbeg + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
+#pragma unroll 4
+    for (int64_t ch = ks; ch < chunks; ch += KS) {
+        const int64_t k0 = kbeg + ch * skinny_mma::CHUNK;
+        uint4 bv[2][2], av[NB][2];  // B rows (g, g+8) x halves; A rows (nb*8 + g) x halves
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            bv[0][c] = load16(Bu, ldb, N, n0 + g, k0 + c * 64 + t * 16, true);
+            bv[1][c] = load16(Bu, ldb, N, n0 + g + 8, k0 + c * 64 + t * 16, true);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) av[nb][c] = load16(A, lda, M, nb * 8 + g, k0 + c * 64 + t * 16, false);
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const uint32_t ba[4] = {bv[0][c].x, bv[0][c].y, bv[0][c].z, bv[0][c].w};
+            const uint32_t bb[4] = {bv[1][c].x, bv[1][c].y, bv[1][c].z, bv[1][c].w};
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+                const uint32_t aa[4] = {av[nb][c].x, av[nb][c].y, av[nb][c].z, av[nb][c].w};
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    mma_u8s8_m16n8k32(d[nb], ba[2 * j], bb[2 * j], ba[2 * j + 1], bb[2 * j + 1], aa[2 * j],
+                                      aa[2 * j + 1]);
+            }
+        }
+    }
+
+    // meet the KS warps of this row group in smem: red[rg][ks][16 rows][MT cols]
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        const int col = nb * 8 + t * 2;
+        int32_t* r0 = red + ((rg * KS + ks) * 16 + g) * MT + col;
+        int32_t* r8 = red + ((rg * KS + ks) * 16 + g + 8) * MT + col;
+        r0[0] = d[nb][0];
+        r0[1] = d[nb][1];
+        r8[0] = d[nb][2];
+        r8[1] = d[nb][3];
+    }
+    __syncthreads();
+    for (int i = tid; i < RG * 16 * MT; i += WARPS * 32) {
+        const int m = i / (RG * 16), rr = i % (RG * 16);  // consecutive threads -> consecutive n
+        const int r_g = rr / 16, row = rr % 16;
+        uint32_t s = 0;
+#pragma unroll
+        for (int q = 0; q < KS; ++q) s += static_cast<uint32_t>(red[((r_g * KS + q) * 16 + row) * MT + m]);
+        const int64_t n = (static_cast<int64_t>(blockIdx.x) * RG + r_g) * 16 + row;
+        if (m < M && n < N) {
+            int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;
+            if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
+            else *dst = static_cast<int32_t>(s);
+        }
+    }
+}
+
+}  // namespace ngemm_dev

@@ -378,6 +378,43 @@ ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, in
     return s;
 }
 
+// Warp-MMA load-stream variant (skinny_mma_kernel, exact mode): 16 B-rows per row group, the
+// CTA's 8/16/32 warps split K so that ~32 warps per SM are streaming; a grid K split (atomic
+// wrap-add into a zeroed C) only when even 32 warps per row group are not enough.
+template <int MT, int WARPS>
+ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
+                                 cudaStream_t st) {
+    const int64_t groups = (n + 15) / 16;
+    const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
+    splits = (k + k_range - 1) / k_range;
+    if (splits > 1) {
+        ngemm_status zs = zero_c(c, ldc, m, n, nullptr, 0, di, st);
+        if (zs != NGEMM_OK) return zs;
+    }
+    const int vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0);
+    NG_LAUNCH(skinny_mma_kernel<MT, 1, WARPS>, dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)),
+              dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
+              splits > 1 ? 1 : 0);
+    return NGEMM_OK;
+}
+
+template <int MT>
+ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    const int64_t groups = (n + 15) / 16;
+    const int64_t chunks = (k + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
+    const int64_t warps_target = static_cast<int64_t>(di.sms) * 32;
+    const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (warps_target + groups - 1) / groups));
+    int64_t splits = 1;
+    if (const char* f = std::getenv("NGEMM_SKINNY_SPLITS")) splits = std::max(1, std::atoi(f));
+    if (ks <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
+    if (ks <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
+    if (ks > 32 && splits == 1) splits = (ks + 31) / 32;
+    return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
+}
+
 // Lanes-own-rows variant (skinny_rows_kernel): 32-row tiles of B x K splits.
 template <int MODE, int MT>
 ngemm_status launch_skinny_rows_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
@@ -418,12 +455,16 @@ ngemm_status launch_skinny_rows_mode(const uint8_t* a, int64_t lda, const int8_t
 ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                            int64_t m, int64_t n, int64_t k, int mode, const DevInfo& di, cudaStream_t st) {
     if (m > kSkinnyMaxM) return fail(NGEMM_ERR_UNSUPPORTED, "skinny path needs M <= 16");
-    // Measured on B200 (profiles/sweep_skinny*.log): exact -> tensor-core swap-AB (2) on every
-    // c2 shape; saturating -> lanes-own-rows broadcast dp4a (1), except M = 1 with short K
-    // where the warp-butterfly variant (0) has the shorter latency chain.
-    int variant = mode == NGEMM_SAT_EXACT ? 2 : ((m == 1 && k <= 1024) ? 0 : 1);
+    // Measured on B200 (profiles/sweep_r1_skinny*.log): exact -> the warp-MMA load stream (3),
+    // fastest on 11 of the 12 c2 shapes (1.9-4.5 us; the tcgen05 swap-AB kernel (2) pays
+    // ~1 us more for TMEM/mbarrier/cluster setup); saturating -> lanes-own-rows broadcast dp4a
+    // (1), except M = 1 with short K where the warp-butterfly variant (0) is shorter.
+    int variant = mode == NGEMM_SAT_EXACT ? 3 : ((m == 1 && k <= 1024) ? 0 : 1);
     if (const char* v = std::getenv("NGEMM_SKINNY_VARIANT")) variant = std::atoi(v);  // experiments
     if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (variant == 3 && mode == NGEMM_SAT_EXACT)
+        return m <= 8 ? launch_skinny_mma_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
+                      : launch_skinny_mma_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     if (variant == 0) {
         if (!skinny_fits(m, k)) return fail(NGEMM_ERR_UNSUPPORTED, "skinny butterfly variant needs A resident in smem");
         return mode == NGEMM_SAT_EXACT ? launch_skinny_mode<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st)

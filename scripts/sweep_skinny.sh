@@ -7,5 +7,5 @@ for l in sys.stdin:
         print(f\"v=$V {d['config']['M']}x{d['config']['N']}x{d['config']['K']} {d['config']['mode']:5s} {d['ms_per_step']*1000:8.2f} us  {r['achieved']:8.1f} GB/s frac={r['frac']}\")
     elif 'Error' in l or 'error' in l: print(l.strip())
 "; }
-for V in 0 1 2; do export NGEMM_SKINNY_VARIANT=$V
-for m in 1 4 16; do for nk in 768x768 3072x768 768x3072 4096x1024; do run ${m}x${nk} exact; [ $V != 2 ] && run ${m}x${nk} sat; done; done; done
+for V in ${VARIANTS:-0 1 2}; do export NGEMM_SKINNY_VARIANT=$V
+for m in 1 4 16; do for nk in 768x768 3072x768 768x3072 4096x1024; do run ${m}x${nk} exact; [ $V -lt 2 ] && run ${m}x${nk} sat; done; done; done
