@@ -68,7 +68,11 @@ struct TileMap {
     }
 };
 
-template <int BN, int STAGES, int CG>
+// MC = 2 (CG = 2 only): a cluster of two CTA pairs computes two horizontally adjacent
+// 256 x BN tiles that share the same A rows; each CTA loads half of its A slab and multicasts
+// it to its counterpart in the other pair, halving A's L2->SM traffic.  The pairs run in
+// lockstep: every CTA's empty barrier waits for both pairs' MMA commits.
+template <int BN, int STAGES, int CG, int MC = 1>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
@@ -91,9 +95,15 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const uint32_t rank = (CG == 2) ? cluster_ctarank() : 0;  // 0 = pair leader
-    const int unit = (CG == 2) ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
-    const int num_units = (CG == 2) ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+    static_assert(MC == 1 || CG == 2, "A multicast pairs need cta_group::2");
+    constexpr int CL = CG * MC;  // CTAs per cluster
+    const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0;
+    const uint32_t rank = crank & (CG - 1);           // rank within the pair: 0 = pair leader
+    const uint32_t pair = crank / CG;                 // which pair of the cluster (MC = 2)
+    const uint32_t leader = pair * CG;                // cluster rank of this pair's leader
+    const uint16_t pair_mask = static_cast<uint16_t>(((1u << CG) - 1u) << leader);
+    const int unit = static_cast<int>(blockIdx.x) / CL;
+    const int num_units = static_cast<int>(gridDim.x) / CL;
     const int num_tiles = map.tiles_m * map.tiles_n * map.splits;
     const int kb_per_split = (num_kb_total + map.splits - 1) / map.splits;
 
@@ -104,7 +114,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         if (c_mode != 2) tma_prefetch(&tma_c);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], 1);
+            mbar_init(&empty[s], MC);  // one commit per pair that reads this stage
         }
         for (int s = 0; s < 2; ++s) {
             mbar_init(&tfull[s], 1);
@@ -114,7 +124,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
     if (warp == 2) tmem_alloc<CG>(tmem_slot, S::TMEM_COLS);
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if constexpr (CL > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
     pdl_wait();  // operands / C may belong to the preceding kernel in the stream
@@ -128,6 +138,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             for (int t = unit; t < num_tiles; t += num_units) {
                 int tm, tn, ks;
                 map.coords(t, tm, tn, ks);
+                tn = tn * MC + static_cast<int>(pair);
                 const int kb0 = ks * kb_per_split;
                 const int kb1 = min(num_kb_total, kb0 + kb_per_split);
                 const int row_a = tm * UMMA_M + static_cast<int>(rank) * tc::BM;
@@ -143,7 +154,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     } else {
                         // both CTAs' bytes land on the leader's full barrier; the leader arms it
                         if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
-                        tma_load_2d_cg2(sa, &tma_a, &full[s], kb * tc::BK, row_a, pol);
+                        if constexpr (MC == 1) {
+                            tma_load_2d_cg2(sa, &tma_a, &full[s], kb * tc::BK, row_a, pol);
+                        } else {
+                            // this CTA's half of the shared A slab, to itself and its counterpart
+                            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
+                            tma_load_2d_cg2_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[s], kb * tc::BK,
+                                               row_a + static_cast<int>(pair) * (tc::BM / 2), mask, pol);
+                        }
                         tma_load_2d_cg2(sb, &tma_b, &full[s], kb * tc::BK, row_b, pol);
                     }
                     if (++s == STAGES) { s = 0; ph ^= 1; }
@@ -177,11 +195,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                                    idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     }
                     if constexpr (CG == 1) mma_commit(&empty[s]);
-                    else mma_commit_cg2_mc(&empty[s], 0x3);
+                    else mma_commit_cg2_mc(&empty[s], MC == 1 ? pair_mask : static_cast<uint16_t>(0xF));
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }
                 if constexpr (CG == 1) mma_commit(&tfull[acc]);
-                else mma_commit_cg2_mc(&tfull[acc], 0x3);
+                else mma_commit_cg2_mc(&tfull[acc], pair_mask);
                 acc ^= 1;
                 if (acc == 0) acc_ph ^= 1;
             }
@@ -195,6 +213,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         for (int t = unit; t < num_tiles; t += num_units) {
             int tm, tn, ks;
             map.coords(t, tm, tn, ks);
+            tn = tn * MC + static_cast<int>(pair);
             const int kb0 = ks * kb_per_split;
             const bool has_k = kb0 < num_kb_total;
             mbar_wait(&tfull[acc], acc_ph);
@@ -240,7 +259,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             __syncwarp();
             if (lane == 0) {
                 if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
-                else mbar_arrive_cluster(&tempty[acc], 0);
+                else mbar_arrive_cluster(&tempty[acc], leader);
             }
             acc ^= 1;
             if (acc == 0) acc_ph ^= 1;
@@ -249,7 +268,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     }
 
     tc_fence_before();
-    if constexpr (CG == 2) cluster_sync(); else __syncthreads();
+    if constexpr (CL > 1) cluster_sync(); else __syncthreads();
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, S::TMEM_COLS);

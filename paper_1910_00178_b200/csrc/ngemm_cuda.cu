@@ -491,21 +491,31 @@ ngemm_status make_tmap_c(CUtensorMap* map, const int32_t* c, int64_t rows, int64
 }
 
 // Tile configurations of the tcgen05 kernel (per CTA: 128 rows of A; cta_group::2 pairs two SMs).
-enum TcCfg { TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_NUM_CFG = 4 };
+enum TcCfg { TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_QUAD256 = 4, TC_NUM_CFG = 5 };
 struct TcCfgInfo {
-    int cg, bn;
+    int cg, bn, mc;
     double cycles_per_kb;  // MMA issue floor per 128-byte K slab, with the smem-bandwidth cap
 };
 constexpr TcCfgInfo kTcCfg[TC_NUM_CFG] = {
-    {2, 256, 512.0},  // 256x256x128 int8 per pair at 8192 MAC/clk/SM
-    {1, 256, 520.0},  // 128x256: 96 B/clk of smem operand reads
-    {1, 128, 300.0},  // 128x128: 128 B/clk, at the smem port limit
-    {1, 64, 192.0},   // 128x64 : smem-bound (192 B/clk needed)
+    {2, 256, 1, 512.0},  // 256x256x128 int8 per pair at 8192 MAC/clk/SM
+    {1, 256, 1, 520.0},  // 128x256: 96 B/clk of smem operand reads
+    {1, 128, 1, 300.0},  // 128x128: 128 B/clk, at the smem port limit
+    {1, 64, 1, 192.0},   // 128x64 : smem-bound (192 B/clk needed)
+    {2, 256, 2, 512.0},  // two pairs sharing A (multicast): 256x512 per 4-CTA cluster
 };
 
 struct TcPlan {
     int cfg, splits;
 };
+
+// The 4-CTA A-multicast configuration is correct (tests force it) but measured 37% slower on
+// 16384^3 (profiles/quad_bench_r1.log: 4-CTA clusters leave SMs idle — 132 of 148 usable — and
+// the two pairs' pipelines run in lockstep), so the planner only considers it with
+// NGEMM_TC_QUAD=1.
+bool quad_disabled() {
+    const char* e = std::getenv("NGEMM_TC_QUAD");
+    return !(e && e[0] == '1');
+}
 
 // Picks the configuration with the smallest estimated makespan (waves x K-loop + epilogue),
 // then adds split-K (TMA reduce-add) while waves stay under one and K is deep.
@@ -515,8 +525,10 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
     double best_t = 1e30;
     for (int cfg = 0; cfg < TC_NUM_CFG; ++cfg) {
         const TcCfgInfo& ci = kTcCfg[cfg];
-        const int64_t tiles = ((m + 128 * ci.cg - 1) / (128 * ci.cg)) * ((n + ci.bn - 1) / ci.bn);
-        const int64_t units = sms / ci.cg;
+        const int64_t tiles_n = (n + ci.bn - 1) / ci.bn;
+        if (ci.mc > 1 && (tiles_n % ci.mc != 0 || quad_disabled())) continue;
+        const int64_t tiles = ((m + 128 * ci.cg - 1) / (128 * ci.cg)) * tiles_n / ci.mc;
+        const int64_t units = sms / (ci.cg * ci.mc);
         for (int splits = 1; splits <= 16; splits *= 2) {
             if (splits > 1 && (!c_mode_ok || num_kb < 4 * splits || tiles * splits > units)) break;
             const int64_t work = tiles * splits;
@@ -525,6 +537,7 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
             double t = static_cast<double>(waves) * kb * ci.cycles_per_kb + 600.0 + ci.bn * 8.0;
             if (splits > 1) t += 1500.0;                 // zeroing C + reduce-add traffic
             if (ci.cg == 2) t *= 0.97;                    // less L2->SM traffic per MAC
+            if (ci.mc == 2) t *= 0.98;                    // A multicast: a further 25% less
             if (t < best_t) {
                 best_t = t;
                 best = {cfg, splits};
@@ -532,16 +545,18 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
         }
     }
     if (const char* force = std::getenv("NGEMM_TC_CFG")) best.cfg = std::atoi(force) % TC_NUM_CFG;  // experiments
+    if (kTcCfg[best.cfg].mc > 1 && ((n + kTcCfg[best.cfg].bn - 1) / kTcCfg[best.cfg].bn) % kTcCfg[best.cfg].mc != 0)
+        best.cfg = TC_PAIR256;  // multicast pairs need an even number of N tiles
     if (const char* force = std::getenv("NGEMM_TC_SPLITS")) best.splits = std::max(1, std::atoi(force));
     return best;
 }
 
-template <int BN, int STAGES, int CG>
+template <int BN, int STAGES, int CG, int MC = 1>
 ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcmap, int32_t* c,
                          int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int c_mode, const DevInfo& di,
                          cudaStream_t st, const int32_t* guard) {
     using S = tc::Smem<BN, STAGES, CG>;
-    auto kern = tc_gemm_kernel<BN, STAGES, CG>;
+    auto kern = tc_gemm_kernel<BN, STAGES, CG, MC>;
     static std::once_flag once[64];
     int dev = 0;
     cudaGetDevice(&dev);
@@ -550,10 +565,10 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     if (s != NGEMM_OK) return s;
     TileMap map;
     map.tiles_m = static_cast<int>((m + tc::BM * CG - 1) / (tc::BM * CG));
-    map.tiles_n = static_cast<int>((n + BN - 1) / BN);
+    map.tiles_n = static_cast<int>((n + BN - 1) / BN) / MC;  // MC adjacent N tiles per cluster
     const int num_kb = static_cast<int>((k + tc::BK - 1) / tc::BK);
     const int tiles = map.tiles_m * map.tiles_n;
-    const int units = di.sms / CG;
+    const int units = di.sms / (CG * MC);
     // split-K needs the TMA reduce-add epilogue (C must be TMA-describable)
     map.splits = c_mode == 2 ? 1 : std::max(1, std::min(splits, num_kb));
     map.group_m = tc::GROUP_M;
@@ -563,8 +578,8 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         ngemm_status zs = zero_c(c, ldc, m, n, guard, 1, di, st);
         if (zs != NGEMM_OK) return zs;
     }
-    const int grid = std::min(tiles * map.splits, units) * CG;
-    NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
+    const int grid = std::min(tiles * map.splits, units) * CG * MC;
+    NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG * MC, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
               static_cast<int>(n), num_kb, map, c_mode, guard);
     return NGEMM_OK;
 }
@@ -600,7 +615,7 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
     const TcCfgInfo& ci = kTcCfg[plan.cfg];
     CUtensorMap ta, tb, tcm;
     std::memset(&tcm, 0, sizeof tcm);
-    ngemm_status s = make_tmap_u8(&ta, a_use, k, m, lda_use, tc::BK, tc::BM);
+    ngemm_status s = make_tmap_u8(&ta, a_use, k, m, lda_use, tc::BK, tc::BM / ci.mc);
     if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, ci.bn / ci.cg);
     if (s == NGEMM_OK && c_tma) s = make_tmap_c(&tcm, c, m, n, ldc);
     const int c_mode = c_tma ? 0 : 2;
@@ -609,6 +624,7 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
         case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         }
     }

@@ -282,7 +282,7 @@ def test_config5_full_size(cuda, oracle, golden):
         assert torch.equal(lhs, rhs)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
 def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
     """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64), with and without
     split-K (TMA s32 reduce-add), with TMA-store and direct-store epilogues, vs the oracle."""
@@ -290,7 +290,7 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
     for splits in ("1", "2", "3"):
         monkeypatch.setenv("NGEMM_TC_SPLITS", splits)
         for (m, n, k, ldc) in ((300, 520, 1100, None), (256, 256, 2048, 260), (129, 65, 640, None),
-                               (513, 300, 1024, 301)):
+                               (513, 300, 1024, 301), (600, 1024, 700, None), (256, 512, 128, 516)):
             a = oracle.mat_random_u8(m, k, m + cfg)
             b = oracle.mat_random_i8(n, k, n + cfg)
             got = dev_gemm(a, b, EXACT, "tcgen05", ldc=ldc)
