@@ -69,6 +69,7 @@ inline void throw_on_status(ngemm_status s) {
     case NGEMM_ERR_RANGE: throw RangeError(msg);
     case NGEMM_ERR_CORRUPTION: throw CorruptionError(msg);
     case NGEMM_ERR_INDEX: throw IndexError(msg);
+    case NGEMM_ERR_TUNE: throw TuneError(msg);
     default: throw CudaError(msg.empty() ? std::string("CUDA error") : msg);
     }
 }

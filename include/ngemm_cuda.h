@@ -48,7 +48,8 @@ typedef enum {
     NGEMM_ERR_RANGE = 4,       /* RangeError        (common.hpp:87-90) */
     NGEMM_ERR_CORRUPTION = 5,  /* CorruptionError   (common.hpp:109-112) */
     NGEMM_ERR_INDEX = 6,       /* IndexError        (common.hpp:92-95) */
-    NGEMM_ERR_CUDA = 7         /* CUDA runtime failure (Error base class) */
+    NGEMM_ERR_CUDA = 7,        /* CUDA runtime failure (Error base class) */
+    NGEMM_ERR_TUNE = 8         /* TuneError         (common.hpp:124-127) */
 } ngemm_status;
 
 typedef enum {
@@ -149,6 +150,30 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
                                         int32_t* c, int64_t m, int64_t n, int64_t k, int sat_mode,
                                         int gather_device, int32_t** gathered);
 ngemm_status ngemm_cuda_free(void* device_ptr);
+
+/* ---- GPU autotuner (replaces the CPU tile search of tuner.hpp:132-245) -------------------- */
+typedef struct {
+    int64_t m, n, k;
+    int32_t sat_mode;
+    int32_t kernel;          /* NGEMM_KERNEL_* that won */
+    int32_t tc_cfg;          /* tcgen05 tile configuration (-1 = not applicable) */
+    int32_t tc_splits;       /* tcgen05 split-K factor (-1 = not applicable) */
+    int32_t skinny_variant;  /* skinny kernel variant (-1 = not applicable) */
+    double median_ns, min_ns;
+    int32_t trials;
+    int64_t timestamp;       /* seconds since the epoch */
+} ngemm_tune_record;
+
+/* Times every applicable kernel configuration for (m, n, k, sat_mode) on the current device
+ * (seeded full-range operands), verifying each bit-for-bit against the CUDA-core reference
+ * kernel before its timing counts (NGEMM_ERR_TUNE on a mismatch); the fastest becomes the
+ * dispatcher's choice for that shape in this process.  repeats >= 3, warmup >= 1. */
+ngemm_status ngemm_cuda_tune(int64_t m, int64_t n, int64_t k, int sat_mode, int repeats, int warmup,
+                             ngemm_tune_record* out);
+/* Append-only text store, one record per line, last record for a shape wins. */
+ngemm_status ngemm_cuda_tune_store_save(const char* path);
+ngemm_status ngemm_cuda_tune_store_load(const char* path, int* loaded);
+ngemm_status ngemm_cuda_tune_clear(void);
 
 /* ---- introspection ----------------------------------------------------------------------- */
 /* Current CUDA device of the calling thread. */

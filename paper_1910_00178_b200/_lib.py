@@ -20,10 +20,11 @@ EXPORTS = [
     "ngemm_cuda_gemm_packed_host", "ngemm_cuda_shard_rows", "ngemm_cuda_gemm_u8i8_multi", "ngemm_cuda_free",
     "ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error", "ngemm_cuda_pick_kernel",
     "ngemm_cuda_launch_count", "ngemm_cuda_gemm_i16", "ngemm_cuda_gemm_i16_host", "ngemm_cuda_gemm_packed_i16",
-    "ngemm_cuda_gemm_packed_resident_host", "ngemm_cuda_device",
+    "ngemm_cuda_gemm_packed_resident_host", "ngemm_cuda_device", "ngemm_cuda_tune", "ngemm_cuda_tune_store_save",
+    "ngemm_cuda_tune_store_load", "ngemm_cuda_tune_clear",
 ]
 
-OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA = range(8)
+OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA, ERR_TUNE = range(9)
 KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT, KERNEL_SKINNY = range(4)
 KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_TCGEN05: "tcgen05", KERNEL_SIMT: "simt", KERNEL_SKINNY: "skinny"}
 
@@ -33,6 +34,13 @@ class PackedMeta(C.Structure):
                 ("tm", C.c_int64), ("tn", C.c_int64), ("tk", C.c_int64),
                 ("perm", C.c_int32), ("m_orig", C.c_int64), ("k_orig", C.c_int64),
                 ("m_pad", C.c_int64), ("k_pad", C.c_int64)]
+
+
+class TuneRecord(C.Structure):
+    _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("sat_mode", C.c_int32),
+                ("kernel", C.c_int32), ("tc_cfg", C.c_int32), ("tc_splits", C.c_int32),
+                ("skinny_variant", C.c_int32), ("median_ns", C.c_double), ("min_ns", C.c_double),
+                ("trials", C.c_int32), ("timestamp", C.c_int64)]
 
 
 _lock = threading.Lock()
@@ -71,6 +79,10 @@ def load():
         L.ngemm_cuda_gemm_packed_i16.argtypes = [vp, vp, i64, vp, i64, i64, vp]
         L.ngemm_cuda_gemm_packed_resident_host.argtypes = [vp, vp, vp, i64, i32]
         L.ngemm_cuda_device.argtypes = [C.POINTER(i32)]
+        L.ngemm_cuda_tune.argtypes = [i64, i64, i64, i32, i32, i32, C.POINTER(TuneRecord)]
+        L.ngemm_cuda_tune_store_save.argtypes = [C.c_char_p]
+        L.ngemm_cuda_tune_store_load.argtypes = [C.c_char_p, C.POINTER(i32)]
+        L.ngemm_cuda_tune_clear.argtypes = []
         for f in EXPORTS:
             fn = getattr(L, f)
             if f not in ("ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error",
@@ -119,8 +131,13 @@ class CudaError(NgemmError):
     pass
 
 
+class TuneError(NgemmError):
+    pass
+
+
 _ERRORS = {ERR_SHAPE: ShapeError, ERR_UNSUPPORTED: UnsupportedError, ERR_CONFIG: ConfigError,
-           ERR_RANGE: RangeError, ERR_CORRUPTION: CorruptionError, ERR_INDEX: IndexError_, ERR_CUDA: CudaError}
+           ERR_RANGE: RangeError, ERR_CORRUPTION: CorruptionError, ERR_INDEX: IndexError_, ERR_CUDA: CudaError,
+           ERR_TUNE: TuneError}
 
 
 def check(status: int):

@@ -28,7 +28,7 @@ import numpy as np
 
 from . import _lib
 from ._lib import (ConfigError, CorruptionError, CudaError, IndexError_, NgemmError, RangeError, ShapeError,
-                   UnsupportedError, check)
+                   TuneError, UnsupportedError, check)
 
 
 class SatMode(enum.IntEnum):
@@ -340,9 +340,34 @@ def gemm_multi(devices, a: np.ndarray, b: np.ndarray, mode: SatMode) -> np.ndarr
     return c
 
 
+def tune(m: int, n: int, k: int, mode: SatMode, repeats: int = 5, warmup: int = 2) -> dict:
+    """GPU autotuner (the reference's tune(), tuner.hpp:132-175, re-targeted): every applicable
+    kernel configuration is verified bit-for-bit against the CUDA-core reference kernel, then
+    timed (median of `repeats` after `warmup`); the winner becomes the dispatcher's choice for
+    this shape in this process.  Raises TuneError if a candidate mis-computes."""
+    rec = _lib.TuneRecord()
+    check(_lib.load().ngemm_cuda_tune(m, n, k, int(mode), repeats, warmup, C.byref(rec)))
+    return {f: getattr(rec, f) for f, _ in rec._fields_}
+
+
+def tune_store_save(path: str):
+    check(_lib.load().ngemm_cuda_tune_store_save(path.encode()))
+
+
+def tune_store_load(path: str) -> int:
+    n = C.c_int()
+    check(_lib.load().ngemm_cuda_tune_store_load(path.encode(), C.byref(n)))
+    return n.value
+
+
+def tune_clear():
+    check(_lib.load().ngemm_cuda_tune_clear())
+
+
 __all__ = [
     "SatMode", "Engine", "Perm", "KernelShape", "kernel_shape", "TileConfig", "PackedWeight", "pack_weights",
     "unpack_weights", "gemm_conventional", "gemm_ngemm", "gemm_device", "DevicePackedWeight", "repack_device",
     "pick_kernel", "shard_rows", "gemm_multi", "NgemmError", "ShapeError", "UnsupportedError", "ConfigError",
-    "RangeError", "CorruptionError", "IndexError_", "CudaError",
+    "RangeError", "CorruptionError", "IndexError_", "CudaError", "TuneError", "tune", "tune_store_save",
+    "tune_store_load", "tune_clear",
 ]

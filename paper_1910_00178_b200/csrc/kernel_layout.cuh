@@ -131,4 +131,29 @@ __global__ void operand_range_kernel(const uint8_t* __restrict__ a, int64_t lda,
     }
 }
 
+// Deterministic full-range operand fill for the tuner (splitmix64 of the element index).
+__global__ void fill_random_kernel(uint8_t* __restrict__ p, int64_t rows, int64_t cols, int64_t ld, uint64_t seed) {
+    const int64_t total = rows * cols;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        uint64_t z = seed + 0x9E3779B97F4A7C15ull * static_cast<uint64_t>(i + 1);
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        const int64_t r = i / cols;
+        p[r * ld + (i - r * cols)] = static_cast<uint8_t>(z >> 56);
+    }
+}
+
+// Counts elements where x != y (the tuner's verify-before-time, tuner.hpp:155-161).
+__global__ void count_mismatch_kernel(const int32_t* __restrict__ x, const int32_t* __restrict__ y, int64_t n,
+                                      unsigned long long* __restrict__ bad) {
+    unsigned long long local = 0;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+        local += (x[i] != y[i]) ? 1ull : 0ull;
+    for (int o = 16; o > 0; o >>= 1) local += __shfl_xor_sync(0xffffffffu, local, o);
+    if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
+}
+
 }  // namespace ngemm_dev

@@ -13,7 +13,12 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <chrono>
+#include <fstream>
+#include <map>
 #include <mutex>
+#include <sstream>
+#include <tuple>
 #include <string>
 #include <thread>
 #include <utility>
@@ -90,9 +95,12 @@ void keep_pool(int dev) {
     });
 }
 
+void autoload_tune_store();
+
 ngemm_status current_device(int* dev, DevInfo* info) {
     NG_CUDA(cudaGetDevice(dev));
     keep_pool(*dev);
+    autoload_tune_store();
     *info = dev_info(*dev);
     if (info->sms <= 0) return fail(NGEMM_ERR_CUDA, "no CUDA device");
     if (info->cc_major != 10 || info->cc_minor != 0)
@@ -153,6 +161,15 @@ ngemm_status validate(const void* a, int64_t lda, const void* b, int64_t ldb, co
     if (m > INT32_MAX / 2 || n > INT32_MAX / 2) return fail(NGEMM_ERR_SHAPE, "gemm: dimension too large");
     return NGEMM_OK;
 }
+
+// ---------------------------------------------------------------- tuned choices
+// A kernel choice for one (m, n, k, mode): set by ngemm_cuda_tune (or loaded from a tune
+// store) and consulted by the dispatcher before its heuristics.  -1 = planner's default.
+struct Choice {
+    int kernel = NGEMM_KERNEL_AUTO;
+    int tc_cfg = -1, tc_splits = -1, skinny_variant = -1;
+};
+thread_local Choice t_force;  // the choice in effect for the launch being issued on this thread
 
 // ---------------------------------------------------------------- launchers
 // Programmatic dependent launch: consecutive kernels on a stream overlap the next kernel's
@@ -461,6 +478,7 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
     // (1), except M = 1 with short K where the warp-butterfly variant (0) is shorter.
     int variant = mode == NGEMM_SAT_EXACT ? 3 : ((m == 1 && k <= 1024) ? 0 : 1);
     if (const char* v = std::getenv("NGEMM_SKINNY_VARIANT")) variant = std::atoi(v);  // experiments
+    if (t_force.skinny_variant >= 0) variant = t_force.skinny_variant;
     if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     if (variant == 3 && mode == NGEMM_SAT_EXACT)
         return m <= 8 ? launch_skinny_mma_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
@@ -545,9 +563,12 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
         }
     }
     if (const char* force = std::getenv("NGEMM_TC_CFG")) best.cfg = std::atoi(force) % TC_NUM_CFG;  // experiments
+
+    if (const char* force = std::getenv("NGEMM_TC_SPLITS")) best.splits = std::max(1, std::atoi(force));
+    if (t_force.tc_cfg >= 0) best.cfg = t_force.tc_cfg % TC_NUM_CFG;
+    if (t_force.tc_splits >= 1) best.splits = t_force.tc_splits;
     if (kTcCfg[best.cfg].mc > 1 && ((n + kTcCfg[best.cfg].bn - 1) / kTcCfg[best.cfg].bn) % kTcCfg[best.cfg].mc != 0)
         best.cfg = TC_PAIR256;  // multicast pairs need an even number of N tiles
-    if (const char* force = std::getenv("NGEMM_TC_SPLITS")) best.splits = std::max(1, std::atoi(force));
     return best;
 }
 
@@ -674,8 +695,21 @@ int pick(int64_t m, int64_t n, int64_t k, int mode) {
     return NGEMM_KERNEL_SIMT;
 }
 
+bool tuned_lookup(int64_t m, int64_t n, int64_t k, int mode, Choice* out);
+
 ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc, int64_t m,
                       int64_t n, int64_t k, int mode, int kernel, cudaStream_t st) {
+    struct Restore {
+        Choice saved = t_force;
+        ~Restore() { t_force = saved; }
+    } restore;
+    if (kernel == NGEMM_KERNEL_AUTO) {
+        Choice ch;
+        if (tuned_lookup(m, n, k, mode, &ch)) {
+            t_force = ch;
+            kernel = ch.kernel;
+        }
+    }
     const bool auto_kernel = kernel == NGEMM_KERNEL_AUTO;
     ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, mode);
     if (s != NGEMM_OK) return s;
@@ -746,6 +780,50 @@ ngemm_status repack_on(const ngemm_packed_meta* meta, const uint8_t* d_packed, u
     NG_LAUNCH(repack_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, geom_of(meta), d_packed, d_a,
               lda * esize, kwords, esize);
     return NGEMM_OK;
+}
+
+// ---------------------------------------------------------------- tuned table
+// NGEMM_TUNE_STORE=<path>: records saved by an earlier `ngemm tune` are loaded on first use.
+struct TuneKey {
+    int64_t m, n, k;
+    int mode;
+    bool operator<(const TuneKey& o) const {
+        return std::tie(m, n, k, mode) < std::tie(o.m, o.n, o.k, o.mode);
+    }
+};
+std::mutex g_tune_mu;
+std::map<TuneKey, std::pair<Choice, ngemm_tune_record>> g_tuned;
+
+bool tuned_lookup(int64_t m, int64_t n, int64_t k, int mode, Choice* out) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    if (g_tuned.empty()) return false;
+    auto it = g_tuned.find(TuneKey{m, n, k, mode});
+    if (it == g_tuned.end()) return false;
+    *out = it->second.first;
+    return true;
+}
+
+ngemm_status load_store_file(const char* path, int* loaded);
+
+void autoload_tune_store() {
+    static std::once_flag once;
+    std::call_once(once, [] {
+        const char* p = std::getenv("NGEMM_TUNE_STORE");
+        if (p && *p) {
+            std::ifstream probe(p);
+            if (probe) load_store_file(p, nullptr);
+        }
+    });
+}
+
+void tuned_put(const ngemm_tune_record& r) {
+    Choice ch;
+    ch.kernel = r.kernel;
+    ch.tc_cfg = r.tc_cfg;
+    ch.tc_splits = r.tc_splits;
+    ch.skinny_variant = r.skinny_variant;
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tuned[TuneKey{r.m, r.n, r.k, r.sat_mode}] = {ch, r};
 }
 
 }  // namespace
@@ -898,6 +976,7 @@ const char* ngemm_cuda_status_name(int s) {
     case NGEMM_ERR_CORRUPTION: return "CorruptionError";
     case NGEMM_ERR_INDEX: return "IndexError";
     case NGEMM_ERR_CUDA: return "CudaError";
+    case NGEMM_ERR_TUNE: return "TuneError";
     default: return "unknown";
     }
 }
@@ -1145,6 +1224,192 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
         *gathered = full;
         cudaSetDevice(prev);
     }
+    return NGEMM_OK;
+}
+
+// ---------------------------------------------------------------- GPU autotuner (tuner.hpp:132-245)
+// Exhaustive search over the engine's own knobs for one (m, n, k, mode) on the current device:
+// seeded full-range operands, every candidate verified bit-for-bit against the CUDA-core
+// kernel (the lane-faithful Engine::Emulated path) before its timing counts; median of
+// `repeats` CUDA-event timings after `warmup` runs; the winner is recorded in the in-process
+// table the dispatcher consults (and can be persisted with ngemm_cuda_tune_store_save).
+ngemm_status ngemm_cuda_tune(int64_t m, int64_t n, int64_t k, int sat_mode, int repeats, int warmup,
+                             ngemm_tune_record* out) {
+    if (repeats < 3 || warmup < 1) return fail(NGEMM_ERR_CONFIG, "tune: repeats must be >= 3 and warmup >= 1");
+    int dev;
+    DevInfo di;
+    ngemm_status s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    s = validate(reinterpret_cast<void*>(1), k, reinterpret_cast<void*>(1), k, reinterpret_cast<void*>(1), n, m, n, k,
+                 sat_mode);
+    if (s != NGEMM_OK) return s;
+    const int64_t kp = round_up(k, 16);
+    const size_t a_b = static_cast<size_t>(m * kp), b_b = static_cast<size_t>(n * kp), c_b = static_cast<size_t>(m * n) * 4;
+    const size_t b_off = round_up(static_cast<int64_t>(a_b), 256), c0 = b_off + round_up(static_cast<int64_t>(b_b), 256),
+                 c1 = c0 + round_up(static_cast<int64_t>(c_b), 256), bad_off = c1 + round_up(static_cast<int64_t>(c_b), 256);
+    uint8_t* buf = nullptr;
+    NG_CUDA(cudaMalloc(&buf, bad_off + 64));
+    cudaStream_t st = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    uint8_t* da = buf;
+    int8_t* db = reinterpret_cast<int8_t*>(buf + b_off);
+    int32_t* cref = reinterpret_cast<int32_t*>(buf + c0);
+    int32_t* ctry = reinterpret_cast<int32_t*>(buf + c1);
+    auto* bad = reinterpret_cast<unsigned long long*>(buf + bad_off);
+    cudaMemset(buf, 0, bad_off + 64);
+    fill_random_kernel<<<di.sms * 4, 256, 0, st>>>(da, m, k, kp, 0x4E47454D4D31ull);
+    fill_random_kernel<<<di.sms * 4, 256, 0, st>>>(reinterpret_cast<uint8_t*>(db), n, k, kp, 0x4E47454D4D32ull);
+    g_launches.fetch_add(2, std::memory_order_relaxed);
+    s = run_gemm(da, kp, db, kp, cref, n, m, n, k, sat_mode, NGEMM_KERNEL_SIMT, st);  // the reference result
+
+    std::vector<Choice> cands;
+    if (m <= kSkinnyMaxM) {
+        for (int v = 0; v < 4; ++v) {
+            if (sat_mode != NGEMM_SAT_EXACT && v >= 2) continue;
+            Choice c;
+            c.kernel = NGEMM_KERNEL_SKINNY;
+            c.skinny_variant = v;
+            cands.push_back(c);
+        }
+    } else if (sat_mode == NGEMM_SAT_EXACT) {
+        for (int cfg = 0; cfg < TC_NUM_CFG; ++cfg) {
+            const TcCfgInfo& ci = kTcCfg[cfg];
+            if (ci.mc > 1 && ((n + ci.bn - 1) / ci.bn) % ci.mc != 0) continue;
+            for (int sp : {1, 2, 4}) {
+                if (sp > 1 && (k + tc::BK - 1) / tc::BK < 4 * sp) continue;
+                Choice c;
+                c.kernel = NGEMM_KERNEL_TCGEN05;
+                c.tc_cfg = cfg;
+                c.tc_splits = sp;
+                cands.push_back(c);
+            }
+        }
+    }
+    {
+        Choice c;
+        c.kernel = NGEMM_KERNEL_SIMT;
+        cands.push_back(c);
+        if (sat_mode != NGEMM_SAT_EXACT && m > kSkinnyMaxM) {
+            Choice p;  // the range-proof dispatcher (tensor cores when inputs cannot saturate)
+            p.kernel = NGEMM_KERNEL_AUTO;
+            cands.push_back(p);
+        }
+    }
+    ngemm_tune_record best{};
+    best.median_ns = 1e30;
+    for (const Choice& c : cands) {
+        if (s != NGEMM_OK) break;
+        struct Restore {
+            Choice saved = t_force;
+            ~Restore() { t_force = saved; }
+        } restore;
+        t_force = c;
+        auto once = [&]() { return run_gemm(da, kp, db, kp, ctry, n, m, n, k, sat_mode, c.kernel, st); };
+        cudaMemsetAsync(ctry, 0x5A, c_b, st);
+        s = once();
+        if (s != NGEMM_OK) break;
+        cudaMemsetAsync(bad, 0, 8, st);
+        count_mismatch_kernel<<<di.sms * 4, 256, 0, st>>>(cref, ctry, m * n, bad);
+        unsigned long long nbad = 0;
+        cudaMemcpy(&nbad, bad, 8, cudaMemcpyDeviceToHost);
+        if (nbad) {
+            s = fail(NGEMM_ERR_TUNE, "tune: candidate kernel=" + std::to_string(c.kernel) + " cfg=" +
+                                         std::to_string(c.tc_cfg) + " splits=" + std::to_string(c.tc_splits) +
+                                         " variant=" + std::to_string(c.skinny_variant) + " disagrees with the "
+                                         "reference kernel on " + std::to_string(nbad) + " elements");
+            break;
+        }
+        for (int w = 0; w < warmup && s == NGEMM_OK; ++w) s = once();
+        std::vector<float> t;
+        for (int r = 0; r < repeats && s == NGEMM_OK; ++r) {
+            cudaEventRecord(e0, st);
+            s = once();
+            cudaEventRecord(e1, st);
+            cudaEventSynchronize(e1);
+            float ms = 0;
+            cudaEventElapsedTime(&ms, e0, e1);
+            t.push_back(ms);
+        }
+        if (s != NGEMM_OK) break;
+        std::sort(t.begin(), t.end());
+        const double med = (t.size() % 2 ? t[t.size() / 2] : 0.5 * (t[t.size() / 2 - 1] + t[t.size() / 2])) * 1e6;
+        if (med < best.median_ns) {
+            best.kernel = c.kernel;
+            best.tc_cfg = c.tc_cfg;
+            best.tc_splits = c.tc_splits;
+            best.skinny_variant = c.skinny_variant;
+            best.median_ns = med;
+            best.min_ns = t.front() * 1e6;
+        }
+    }
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(buf);
+    if (s != NGEMM_OK) return s;
+    best.m = m;
+    best.n = n;
+    best.k = k;
+    best.sat_mode = sat_mode;
+    best.trials = repeats;
+    best.timestamp = static_cast<int64_t>(std::chrono::duration_cast<std::chrono::seconds>(
+                                              std::chrono::system_clock::now().time_since_epoch())
+                                              .count());
+    tuned_put(best);
+    if (out) *out = best;
+    return NGEMM_OK;
+}
+
+// Tune store (tuner.hpp:177-245 style): one record per line, fixed field order, append-only,
+// last record for a key wins:  m n k mode kernel tc_cfg tc_splits skinny_variant median_ns min_ns trials timestamp
+ngemm_status ngemm_cuda_tune_store_save(const char* path) {
+    if (!path) return fail(NGEMM_ERR_CONFIG, "tune store: null path");
+    std::ofstream f(path, std::ios::app);
+    if (!f) return fail(NGEMM_ERR_CONFIG, std::string("tune store: cannot open ") + path);
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    for (const auto& kv : g_tuned) {
+        const ngemm_tune_record& r = kv.second.second;
+        f << r.m << ' ' << r.n << ' ' << r.k << ' ' << r.sat_mode << ' ' << r.kernel << ' ' << r.tc_cfg << ' '
+          << r.tc_splits << ' ' << r.skinny_variant << ' ' << r.median_ns << ' ' << r.min_ns << ' ' << r.trials << ' '
+          << r.timestamp << '\n';
+    }
+    return f ? NGEMM_OK : fail(NGEMM_ERR_CONFIG, "tune store: write failed");
+}
+
+ngemm_status ngemm_cuda_tune_store_load(const char* path, int* loaded) { return load_store_file(path, loaded); }
+
+}  // extern "C"
+
+namespace {
+ngemm_status load_store_file(const char* path, int* loaded) {
+    if (!path) return fail(NGEMM_ERR_CONFIG, "tune store: null path");
+    std::ifstream f(path);
+    if (!f) return fail(NGEMM_ERR_CONFIG, std::string("tune store: cannot open ") + path);
+    std::string line;
+    int count = 0, lineno = 0;
+    while (std::getline(f, line)) {
+        ++lineno;
+        if (line.empty() || line[0] == '#') continue;
+        std::istringstream is(line);
+        ngemm_tune_record r{};
+        if (!(is >> r.m >> r.n >> r.k >> r.sat_mode >> r.kernel >> r.tc_cfg >> r.tc_splits >> r.skinny_variant >>
+              r.median_ns >> r.min_ns >> r.trials >> r.timestamp) ||
+            r.m < 1 || r.n < 1 || r.k < 1 || (r.sat_mode != 0 && r.sat_mode != 1) || r.kernel < 0 || r.kernel > 3)
+            return fail(NGEMM_ERR_CONFIG, "tune store: malformed record at line " + std::to_string(lineno));
+        tuned_put(r);
+        ++count;
+    }
+    if (loaded) *loaded = count;
+    return NGEMM_OK;
+}
+}  // namespace
+
+extern "C" {
+
+ngemm_status ngemm_cuda_tune_clear(void) {
+    std::lock_guard<std::mutex> lk(g_tune_mu);
+    g_tuned.clear();
     return NGEMM_OK;
 }
 

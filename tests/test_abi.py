@@ -31,9 +31,9 @@ def test_library_exports_every_declared_symbol():
 def test_abi_version_and_status_names():
     L = _lib.load()
     assert L.ngemm_cuda_abi_version() == 1
-    names = [L.ngemm_cuda_status_name(i).decode() for i in range(8)]
+    names = [L.ngemm_cuda_status_name(i).decode() for i in range(9)]
     assert names == ["ok", "ShapeError", "UnsupportedError", "ConfigError", "RangeError", "CorruptionError",
-                     "IndexError", "CudaError"]
+                     "IndexError", "CudaError", "TuneError"]
 
 
 def test_kernel_pick_policy():
@@ -134,3 +134,24 @@ def test_pack_rejects_bad_tiles_and_kinds():
             api.pack_weights(a, s, t)
     with pytest.raises(api.UnsupportedError):
         api.pack_weights(np.zeros((4, 4), np.int32), s, api.TileConfig(8, 1, 4))
+
+
+def test_tune_store_round_trip_and_malformed(tmp_path):
+    # the store is host-side (no GPU needed): append-only lines, last record for a shape wins
+    p = tmp_path / "tune.txt"
+    p.write_text("# m n k mode kernel cfg splits variant median min trials ts\n"
+                 "1024 1024 1024 1 1 3 1 -1 5000 4800 5 1700000000\n"
+                 "1024 1024 1024 1 1 2 2 -1 4000 3900 5 1700000001\n"
+                 "16 4096 1024 1 3 -1 -1 3 3000 2900 5 1700000002\n")
+    api.tune_clear()
+    assert api.tune_store_load(str(p)) == 3
+    out = tmp_path / "saved.txt"
+    api.tune_store_save(str(out))
+    lines = [l.split() for l in out.read_text().splitlines()]
+    assert len(lines) == 2  # last wins per shape
+    assert ["1024", "1024", "1024", "1", "1", "2", "2", "-1"] in [l[:8] for l in lines]
+    bad = tmp_path / "bad.txt"
+    bad.write_text("1024 1024 x\n")
+    with pytest.raises(api.ConfigError):
+        api.tune_store_load(str(bad))
+    api.tune_clear()
