@@ -8,7 +8,14 @@ LIB := $(PKG)/lib/libngemm_cuda.so
 NVFLAGS := -gencode arch=compute_100a,code=sm_100a -O3 -lineinfo -std=c++17 \
            -Xcompiler -fPIC -Xcompiler -Wall -shared -Iinclude -I$(CSRC) --expt-relaxed-constexpr
 
-all: $(LIB) oracle
+CLI := bin/ngemm
+
+all: $(LIB) $(CLI) oracle
+
+$(CLI): tools/ngemm_cli.cpp $(wildcard include/ngemm/*.hpp) include/ngemm_cuda.h $(LIB)
+	mkdir -p bin
+	g++ -std=c++20 -O2 -Wall -Wextra -Iinclude -o $@ tools/ngemm_cli.cpp -L$(PKG)/lib -lngemm_cuda \
+	    -Wl,-rpath,'$$ORIGIN/../$(PKG)/lib'
 
 $(LIB): $(wildcard $(CSRC)/*.cu $(CSRC)/*.cuh) include/ngemm_cuda.h
 	mkdir -p $(PKG)/lib
@@ -24,7 +31,7 @@ sass:
 	/usr/local/cuda/bin/cuobjdump -sass $(LIB) > /tmp/ngemm.sass && grep -cE "UTCIMMA|UTMALDG|LDTM|IDP" /tmp/ngemm.sass
 
 clean:
-	rm -f $(LIB)
+	rm -f $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
 .PHONY: all oracle ptxas sass clean
