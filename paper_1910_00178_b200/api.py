@@ -326,8 +326,10 @@ def shard_rows(m: int, ndev: int, align: int = 128):
     return list(out)
 
 
-def gemm_multi(devices, a: np.ndarray, b: np.ndarray, mode: SatMode) -> np.ndarray:
-    """Single-process M-shard over `devices` (host arrays), B replicated, no collective."""
+def gemm_multi(devices, a: np.ndarray, b: np.ndarray, mode: SatMode, gather_device: int = -1):
+    """Single-process M-shard over `devices` (host arrays), B replicated, no collective.
+    Returns C on the host; with gather_device >= 0 also returns the device pointer of the
+    full C assembled on that device by peer copies (free with ngemm_cuda_free)."""
     a = np.ascontiguousarray(a)
     b = np.ascontiguousarray(b)
     _check_operands(a, b)
@@ -335,9 +337,11 @@ def gemm_multi(devices, a: np.ndarray, b: np.ndarray, mode: SatMode) -> np.ndarr
     n = b.shape[0]
     c = np.empty((m, n), np.int32)
     devs = (C.c_int * len(devices))(*devices)
+    g = C.c_void_p()
     check(_lib.load().ngemm_cuda_gemm_u8i8_multi(devs, len(devices), a.ctypes.data, b.ctypes.data, c.ctypes.data,
-                                                   m, n, k, int(mode), -1, None))
-    return c
+                                                   m, n, k, int(mode), gather_device,
+                                                   C.byref(g) if gather_device >= 0 else None))
+    return (c, g.value) if gather_device >= 0 else c
 
 
 def tune(m: int, n: int, k: int, mode: SatMode, repeats: int = 5, warmup: int = 2) -> dict:

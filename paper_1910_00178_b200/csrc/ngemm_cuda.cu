@@ -1189,41 +1189,89 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
                                         int64_t m, int64_t n, int64_t k, int sat_mode, int gather_device,
                                         int32_t** gathered) {
     if (!devices || ndev < 1) return fail(NGEMM_ERR_CONFIG, "multi: empty device list");
-    ngemm_status s = validate(a, k, b, k, c, n, m, n, k, sat_mode);
+    const bool want_gather = gather_device >= 0 && gathered != nullptr;
+    if (!c && !want_gather) return fail(NGEMM_ERR_SHAPE, "multi: no output (host C and gather both absent)");
+    ngemm_status s = validate(a, k, b, k, c ? static_cast<const void*>(c) : static_cast<const void*>(a), n, m, n, k,
+                              sat_mode);
     if (s != NGEMM_OK) return s;
     std::vector<int64_t> rs(static_cast<size_t>(ndev) + 1);
     ngemm_cuda_shard_rows(m, ndev, tc::BM, rs.data());
+    int prev = 0;
+    cudaGetDevice(&prev);
+    int32_t* full = nullptr;
+    if (want_gather) {
+        NG_CUDA(cudaSetDevice(gather_device));
+        NG_CUDA(cudaMalloc(&full, static_cast<size_t>(m * n) * 4));
+    }
+    // One host thread per device: H2D of the row shard of A and a replica of B, the GEMM on the
+    // device's own stream, then C rows to the host and/or peer-copied (NVLink) into the gather
+    // buffer — shards of row-major C are contiguous, so the gather is a pure concatenation.
     std::vector<ngemm_status> st(static_cast<size_t>(ndev), NGEMM_OK);
     std::vector<std::string> msg(static_cast<size_t>(ndev));
     std::vector<std::thread> workers;
     for (int d = 0; d < ndev; ++d) {
         workers.emplace_back([&, d] {
-            const int64_t r0 = rs[d], r1 = rs[d + 1];
-            if (r1 <= r0) return;
-            if (cudaSetDevice(devices[d]) != cudaSuccess) {
-                st[d] = NGEMM_ERR_CUDA;
-                msg[d] = "cudaSetDevice failed";
-                return;
+            const int64_t r0 = rs[d], r1 = rs[d + 1], rows = r1 - r0;
+            if (rows <= 0) return;
+            auto bad = [&](ngemm_status code, const std::string& what) {
+                st[d] = code;
+                msg[d] = what;
+            };
+            if (cudaSetDevice(devices[d]) != cudaSuccess) return bad(NGEMM_ERR_CUDA, "cudaSetDevice failed");
+            int dev;
+            DevInfo di;
+            if (current_device(&dev, &di) != NGEMM_OK) return bad(NGEMM_ERR_CUDA, ngemm_cuda_last_error());
+            const int64_t kp = round_up(k, 16);
+            const size_t a_b = static_cast<size_t>(rows * kp), b_b = static_cast<size_t>(n * kp);
+            const size_t c_b = static_cast<size_t>(rows * n) * 4;
+            const size_t b_off = round_up(static_cast<int64_t>(a_b), 256), c_off = b_off + round_up(static_cast<int64_t>(b_b), 256);
+            cudaStream_t stream = nullptr;
+            if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
+                return bad(NGEMM_ERR_CUDA, "stream create failed");
+            uint8_t* buf = nullptr;
+            ngemm_status ls = NGEMM_OK;
+            if (cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_b, stream) != cudaSuccess) {
+                ls = NGEMM_ERR_CUDA;
+                msg[d] = "device allocation failed";
             }
-            st[d] = ngemm_cuda_gemm_u8i8_host(a + r0 * k, b, c + r0 * n, r1 - r0, n, k, sat_mode, NGEMM_KERNEL_AUTO);
-            if (st[d] != NGEMM_OK) msg[d] = ngemm_cuda_last_error();
+            int32_t* dc = buf ? reinterpret_cast<int32_t*>(buf + c_off) : nullptr;
+            if (ls == NGEMM_OK && (copy_rows_h2d(buf, kp, a + r0 * k, k, rows, stream) != cudaSuccess ||
+                                   copy_rows_h2d(buf + b_off, kp, b, k, n, stream) != cudaSuccess)) {
+                ls = NGEMM_ERR_CUDA;
+                msg[d] = "H2D copy failed";
+            }
+            if (ls == NGEMM_OK) {
+                ls = run_gemm(buf, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp, dc, n, rows, n, k, sat_mode,
+                              NGEMM_KERNEL_AUTO, stream);
+                if (ls != NGEMM_OK) msg[d] = ngemm_cuda_last_error();
+            }
+            if (ls == NGEMM_OK && c &&
+                cudaMemcpyAsync(c + r0 * n, dc, c_b, cudaMemcpyDeviceToHost, stream) != cudaSuccess) {
+                ls = NGEMM_ERR_CUDA;
+                msg[d] = "D2H copy failed";
+            }
+            if (ls == NGEMM_OK && full &&
+                cudaMemcpyPeerAsync(full + r0 * n, gather_device, dc, devices[d], c_b, stream) != cudaSuccess) {
+                ls = NGEMM_ERR_CUDA;
+                msg[d] = "peer gather copy failed";
+            }
+            if (buf) cudaFreeAsync(buf, stream);
+            if (cudaStreamSynchronize(stream) != cudaSuccess && ls == NGEMM_OK) {
+                ls = NGEMM_ERR_CUDA;
+                msg[d] = cudaGetErrorString(cudaGetLastError());
+            }
+            cudaStreamDestroy(stream);
+            st[d] = ls;
         });
     }
     for (auto& w : workers) w.join();
+    cudaSetDevice(prev);
     for (int d = 0; d < ndev; ++d)
-        if (st[d] != NGEMM_OK) return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
-    if (gather_device >= 0 && gathered) {
-        // Assemble the row-major C on one device: shards are contiguous byte ranges, so the
-        // gather is a concatenation of host->device copies of each shard's rows.
-        int prev = 0;
-        cudaGetDevice(&prev);
-        NG_CUDA(cudaSetDevice(gather_device));
-        int32_t* full = nullptr;
-        NG_CUDA(cudaMalloc(&full, static_cast<size_t>(m * n) * 4));
-        NG_CUDA(cudaMemcpy(full, c, static_cast<size_t>(m * n) * 4, cudaMemcpyHostToDevice));
-        *gathered = full;
-        cudaSetDevice(prev);
-    }
+        if (st[d] != NGEMM_OK) {
+            if (full) cudaFree(full);
+            return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
+        }
+    if (want_gather) *gathered = full;
     return NGEMM_OK;
 }
 

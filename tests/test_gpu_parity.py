@@ -3,6 +3,8 @@ against the CPU oracle (pinned to the reference) and the reference-generated fix
 
 Modes: SAT = HardwareSaturating (gemm_sat_oracle, gemm.hpp:83-104), EXACT = WideningExact
 (gemm_ref, gemm.hpp:36-52).  Integer work: the bar is bit-exact, no tolerance."""
+import os
+
 import numpy as np
 import pytest
 
@@ -252,6 +254,17 @@ def test_multi_device_driver_single_gpu(cuda, oracle):
         assert (api.gemm_multi([0], a, b, mode) == oracle.gemm(a, b, mode)).all()
         # same device listed twice = two row shards on one GPU (host-side shard/concat logic)
         assert (api.gemm_multi([0, 0], a, b, mode) == oracle.gemm(a, b, mode)).all()
+        # gather of the row shards into one device buffer (peer copies; here device 0 -> 0)
+        import ctypes
+        import glob
+        import nvidia.cuda_runtime
+        rt = ctypes.CDLL(glob.glob(os.path.join(list(nvidia.cuda_runtime.__path__)[0], "lib", "libcudart.so*"))[0])
+        rt.cudaMemcpy.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_size_t, ctypes.c_int]
+        c, ptr = api.gemm_multi([0, 0], a, b, mode, gather_device=0)
+        full = np.empty_like(c)
+        assert rt.cudaMemcpy(full.ctypes.data, ptr, full.nbytes, 2) == 0  # cudaMemcpyDeviceToHost
+        assert (full == c).all() and (c == oracle.gemm(a, b, mode)).all()
+        _lib.check(_lib.load().ngemm_cuda_free(ptr))
 
 
 @pytest.mark.slow
