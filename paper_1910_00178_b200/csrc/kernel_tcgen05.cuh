@@ -54,6 +54,7 @@ struct Smem {
 struct TileMap {
     int tiles_m, tiles_n, splits;  // tiles_m counts 128*CG-row tiles
     int group_m;                   // rasterisation: group_m M-tiles walked down before moving along N
+    int preissue;                  // 1-CTA tiles: issue the first STAGES loads before the block sync
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -108,6 +109,55 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const int kb_per_split = (num_kb_total + map.splits - 1) / map.splits;
 
     pdl_launch_dependents();
+
+    // ---------------- TMA producer state (warp 0, one thread; both CTAs of a pair)
+    int p_t = unit, p_kb = 0, p_kb1 = 0, p_s = 0, p_row_a = 0, p_row_b = 0;
+    uint32_t p_ph = 0;
+    bool p_open = false;
+    auto produce = [&](int budget) {
+        const uint64_t pol = policy_evict_normal();
+        while (p_t < num_tiles && budget != 0) {
+            if (!p_open) {
+                int tm, tn, ks;
+                map.coords(p_t, tm, tn, ks);
+                tn = tn * MC + static_cast<int>(pair);
+                p_kb = ks * kb_per_split;
+                p_kb1 = min(num_kb_total, p_kb + kb_per_split);
+                p_row_a = tm * UMMA_M + static_cast<int>(rank) * tc::BM;
+                p_row_b = tn * BN + static_cast<int>(rank) * (BN / CG);
+                p_open = true;
+            }
+            if (p_kb >= p_kb1) {
+                p_t += num_units;
+                p_open = false;
+                continue;
+            }
+            mbar_wait(&empty[p_s], p_ph ^ 1);  // returns at once for the first STAGES fills
+            uint8_t* sa = smem + p_s * S::A_BYTES;
+            uint8_t* sb = smem + STAGES * S::A_BYTES + p_s * S::B_BYTES;
+            if constexpr (CG == 1) {
+                mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
+                tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol);
+                tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol);
+            } else {
+                // both CTAs' bytes land on the leader's full barrier; the leader arms it
+                if (rank == 0) mbar_arrive_expect_tx(&full[p_s], 2 * S::STAGE_BYTES);
+                if constexpr (MC == 1) {
+                    tma_load_2d_cg2(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol);
+                } else {
+                    // this CTA's half of the shared A slab, to itself and its counterpart
+                    const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
+                    tma_load_2d_cg2_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[p_s], p_kb * tc::BK,
+                                       p_row_a + static_cast<int>(pair) * (tc::BM / 2), mask, pol);
+                }
+                tma_load_2d_cg2(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol);
+            }
+            ++p_kb;
+            if (++p_s == STAGES) { p_s = 0; p_ph ^= 1; }
+            --budget;
+        }
+    };
+
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
@@ -121,6 +171,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             mbar_init(&tempty[s], 4 * CG);  // one arrival per epilogue warp of every CTA
         }
         fence_mbar_init();
+        if (CL == 1 && map.preissue) {
+            // single-CTA tiles: start the operand stream before the block-wide sync, so the first
+            // DRAM round trips overlap TMEM allocation and the sync
+            pdl_wait();
+            produce(STAGES);
+        }
     }
     if (warp == 2) tmem_alloc<CG>(tmem_slot, S::TMEM_COLS);
     tc_fence_before();
@@ -130,44 +186,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     pdl_wait();  // operands / C may belong to the preceding kernel in the stream
 
     if (warp == 0) {
-        if (lane == 0) {
-            // ---------------- TMA producer (both CTAs)
-            const uint64_t pol = policy_evict_normal();
-            int s = 0;
-            uint32_t ph = 0;
-            for (int t = unit; t < num_tiles; t += num_units) {
-                int tm, tn, ks;
-                map.coords(t, tm, tn, ks);
-                tn = tn * MC + static_cast<int>(pair);
-                const int kb0 = ks * kb_per_split;
-                const int kb1 = min(num_kb_total, kb0 + kb_per_split);
-                const int row_a = tm * UMMA_M + static_cast<int>(rank) * tc::BM;
-                const int row_b = tn * BN + static_cast<int>(rank) * (BN / CG);
-                for (int kb = kb0; kb < kb1; ++kb) {
-                    mbar_wait(&empty[s], ph ^ 1);
-                    uint8_t* sa = smem + s * S::A_BYTES;
-                    uint8_t* sb = smem + STAGES * S::A_BYTES + s * S::B_BYTES;
-                    if constexpr (CG == 1) {
-                        mbar_arrive_expect_tx(&full[s], S::STAGE_BYTES);
-                        tma_load_2d(sa, &tma_a, &full[s], kb * tc::BK, row_a, pol);
-                        tma_load_2d(sb, &tma_b, &full[s], kb * tc::BK, row_b, pol);
-                    } else {
-                        // both CTAs' bytes land on the leader's full barrier; the leader arms it
-                        if (rank == 0) mbar_arrive_expect_tx(&full[s], 2 * S::STAGE_BYTES);
-                        if constexpr (MC == 1) {
-                            tma_load_2d_cg2(sa, &tma_a, &full[s], kb * tc::BK, row_a, pol);
-                        } else {
-                            // this CTA's half of the shared A slab, to itself and its counterpart
-                            const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
-                            tma_load_2d_cg2_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[s], kb * tc::BK,
-                                               row_a + static_cast<int>(pair) * (tc::BM / 2), mask, pol);
-                        }
-                        tma_load_2d_cg2(sb, &tma_b, &full[s], kb * tc::BK, row_b, pol);
-                    }
-                    if (++s == STAGES) { s = 0; ph ^= 1; }
-                }
-            }
-        }
+        if (lane == 0) produce(-1);
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (single thread of the leader CTA)
