@@ -389,3 +389,136 @@ __global__ void __launch_bounds__(WARPS * 32)
 }
 
 }  // namespace ngemm_dev
+
+namespace ngemm_dev {
+
+// ---------------------------------------------------------------------------------------------
+// skinny_sat_kernel — HardwareSaturating skinny GEMM (M <= 16) with the load-stream layout of
+// skinny_mma_kernel: each warp owns 16 rows of B (lane g of each quad on rows g and g+8) and a K
+// slice; thread t of a quad reads bytes [c*64 + t*16, +16) of each 128-byte chunk (c = 0, 1),
+// so every load is a 16-byte vector and pair boundaries stay even-aligned.  A (<= 16 rows) comes
+// through L1.  Per 4-byte K word: 2 IDP.4A on the masked A halves, each pair sum clamped to
+// int16, wrap-added (accumulated on the FMA pipe).  The quad's four K phases fold with two
+// shuffle levels (transposing, so each lane keeps 1/4 of the values), the CTA's warps meet in
+// shared memory.
+// ---------------------------------------------------------------------------------------------
+template <int MT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32)
+    skinny_sat_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
+                      int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range, int vec_ok,
+                      int accumulate) {
+    constexpr int V = 2 * MT;  // values per thread: rows {g, g+8} x MT
+    __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    pdl_launch_dependents();
+    pdl_wait();
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 16;
+    const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
+    const int32_t one = (K > 0) ? 1 : 0;  // runtime 1 (keeps the adds on the FMA pipe)
+
+    auto load16 = [&](const uint8_t* X, int64_t ld, int64_t rows, int64_t row, int64_t k, bool stream) -> uint4 {
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row >= rows || k >= K) return v;
+        const uint8_t* p = X + row * ld + k;
+        if (vec_ok && k + 16 <= K) {
+            if (stream)
+                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
+                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+            else
+                v = __ldg(reinterpret_cast<const uint4*>(p));
+            return v;
+        }
+        uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int i = 0; i < 16; ++i)
+            if (k + i < K) w[i >> 2] |= static_cast<uint32_t>(__ldg(p + i)) << (8 * (i & 3));
+        return make_uint4(w[0], w[1], w[2], w[3]);
+    };
+
+    int32_t acc[V];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc[i] = 0;
+
+    const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
+    const int64_t chunks = (min(K, kbeg + k_range) - kbeg + 127) / 128;
+#pragma unroll 2
+    for (int64_t ch = warp; ch < chunks; ch += WARPS) {
+        const int64_t k0 = kbeg + ch * 128;  // k_range is a multiple of 128: pairs stay even-aligned
+        uint4 bv[2][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            bv[0][c] = load16(Bu, ldb, N, n0 + g, k0 + c * 64 + t * 16, true);
+            bv[1][c] = load16(Bu, ldb, N, n0 + g + 8, k0 + c * 64 + t * 16, true);
+        }
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const uint4 av = load16(A, lda, M, m, k0 + c * 64 + t * 16, false);
+                const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                for (int r = 0; r < 2; ++r) {
+                    const uint32_t bw[4] = {bv[r][c].x, bv[r][c].y, bv[r][c].z, bv[r][c].w};
+                    int32_t s = acc[r * MT + m];
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const int32_t p0 = clamp_i16(dp4a_us(aw[q] & 0x0000FFFFu, bw[q], 0));
+                        const int32_t p1 = clamp_i16(dp4a_us(aw[q] & 0xFFFF0000u, bw[q], 0));
+                        s = imad_u32(p0, one, imad_u32(p1, one, s));
+                    }
+                    acc[r * MT + m] = s;
+                }
+            }
+        }
+    }
+    // fold the quad's 4 K phases: after offsets 1 and 2 each lane holds V/4 totals
+    int base = 0;
+    {
+        const bool up = (t & 1) != 0;
+#pragma unroll
+        for (int i = 0; i < V / 2; ++i) {
+            const int32_t keep = up ? acc[i + V / 2] : acc[i], send = up ? acc[i] : acc[i + V / 2];
+            acc[i] = static_cast<int32_t>(static_cast<uint32_t>(keep) +
+                                          static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, send, 1)));
+        }
+        if (up) base += V / 2;
+        if constexpr (V >= 4) {
+            const bool up2 = (t & 2) != 0;
+#pragma unroll
+            for (int i = 0; i < V / 4; ++i) {
+                const int32_t keep = up2 ? acc[i + V / 4] : acc[i], send = up2 ? acc[i] : acc[i + V / 4];
+                acc[i] = static_cast<int32_t>(static_cast<uint32_t>(keep) +
+                                              static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, send, 2)));
+            }
+            if (up2) base += V / 4;
+        } else {
+            acc[0] = static_cast<int32_t>(static_cast<uint32_t>(acc[0]) +
+                                          static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, acc[0], 2)));
+        }
+    }
+    // lane (g, t) now holds values base .. base + LEFT - 1 of the index space r * MT + m
+    constexpr int LEFT = V >= 4 ? V / 4 : 1;
+    if (V >= 4 || (t & 2) == 0) {
+#pragma unroll
+        for (int i = 0; i < LEFT; ++i) {
+            const int idx = base + i, r = idx / MT, m = idx - r * MT;
+            red[(warp * 16 + g + 8 * r) * MT + m] = acc[i];
+        }
+    }
+    __syncthreads();
+    for (int i = tid; i < 16 * MT; i += WARPS * 32) {
+        const int m = i / 16, row = i % 16;
+        uint32_t s = 0;
+#pragma unroll
+        for (int w = 0; w < WARPS; ++w) s += static_cast<uint32_t>(red[(w * 16 + row) * MT + m]);
+        const int64_t n = n0 + row;
+        if (m < M && n < N) {
+            int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;
+            if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
+            else *dst = static_cast<int32_t>(s);
+        }
+    }
+}
+
+}  // namespace ngemm_dev

@@ -432,6 +432,42 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
     return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
 }
 
+// Saturating load-stream variant (skinny_sat_kernel): 16 B-rows per CTA, 8/16/32 warps split
+// the K range; the work is CUDA-core (ALU) bound for larger M, so a grid K split (atomic
+// wrap-add into a zeroed C) spreads it over every SM when there are few row groups.
+template <int MT, int WARPS>
+ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
+                                 cudaStream_t st) {
+    const int64_t groups = (n + 15) / 16;
+    const int64_t k_range = round_up((k + splits - 1) / splits, 128);
+    splits = (k + k_range - 1) / k_range;
+    if (splits > 1) {
+        ngemm_status zs = zero_c(c, ldc, m, n, nullptr, 0, di, st);
+        if (zs != NGEMM_OK) return zs;
+    }
+    const int vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0);
+    NG_LAUNCH(skinny_sat_kernel<MT, WARPS>, dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)),
+              dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
+              splits > 1 ? 1 : 0);
+    return NGEMM_OK;
+}
+
+template <int MT>
+ngemm_status launch_skinny_sat_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    const int64_t groups = (n + 15) / 16;
+    const int64_t chunks = (k + 127) / 128;
+    const int64_t want = static_cast<int64_t>(di.sms) * (MT >= 8 ? 16 : 32);  // resident warps to fill
+    const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + groups - 1) / groups));
+    constexpr int WMAX = MT >= 8 ? 16 : 32;  // 1024-thread CTAs cap registers at 64: spills for MT >= 8
+    if (ks <= 8) return launch_skinny_sat_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, 1, di, st);
+    if (ks <= 16 || WMAX == 16)
+        return launch_skinny_sat_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 15) / 16, di, st);
+    return launch_skinny_sat_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 31) / 32, di, st);
+}
+
 // Lanes-own-rows variant (skinny_rows_kernel): 32-row tiles of B x K splits.
 template <int MODE, int MT>
 ngemm_status launch_skinny_rows_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
@@ -474,12 +510,18 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
     if (m > kSkinnyMaxM) return fail(NGEMM_ERR_UNSUPPORTED, "skinny path needs M <= 16");
     // Measured on B200 (profiles/sweep_r1_skinny*.log): exact -> the warp-MMA load stream (3),
     // fastest on 11 of the 12 c2 shapes (1.9-4.5 us; the tcgen05 swap-AB kernel (2) pays
-    // ~1 us more for TMEM/mbarrier/cluster setup); saturating -> lanes-own-rows broadcast dp4a
-    // (1), except M = 1 with short K where the warp-butterfly variant (0) is shorter.
-    int variant = mode == NGEMM_SAT_EXACT ? 3 : ((m == 1 && k <= 1024) ? 0 : 1);
+    // ~1 us more for TMEM/mbarrier/cluster setup); saturating -> the dp4a load stream (4),
+    // except M > 4 with few B rows where the lanes-own-rows broadcast kernel (1) wins.
+    int variant = mode == NGEMM_SAT_EXACT ? 3 : ((m > 4 && n < 2048) ? 1 : 4);
     if (const char* v = std::getenv("NGEMM_SKINNY_VARIANT")) variant = std::atoi(v);  // experiments
     if (t_force.skinny_variant >= 0) variant = t_force.skinny_variant;
     if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    if (variant == 4 && mode != NGEMM_SAT_EXACT) {
+        if (m <= 1) return launch_skinny_sat_t<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+        if (m <= 4) return launch_skinny_sat_t<4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+        if (m <= 8) return launch_skinny_sat_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+        return launch_skinny_sat_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    }
     if (variant == 3 && mode == NGEMM_SAT_EXACT)
         return m <= 8 ? launch_skinny_mma_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
                       : launch_skinny_mma_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);

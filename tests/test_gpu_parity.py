@@ -310,7 +310,7 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
             assert (got == oracle.gemm(a, b, EXACT)).all(), (cfg, splits, m, n, k, ldc)
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
 def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
     """Skinny (M <= 16) variants: 0 warp-butterfly dp4a, 1 lanes-own-rows dp4a (broadcast A),
     2 tensor-core swap-AB, 3 warp-MMA load stream (2 and 3: exact mode only; sat falls back
