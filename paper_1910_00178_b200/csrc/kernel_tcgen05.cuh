@@ -55,6 +55,7 @@ struct TileMap {
     int tiles_m, tiles_n, splits;  // tiles_m counts 128*CG-row tiles
     int group_m;                   // rasterisation: group_m M-tiles walked down before moving along N
     int preissue;                  // 1-CTA tiles: issue the first STAGES loads before the block sync
+    int l2hint;                    // L2 eviction hints: A evict_last, B evict_first
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -115,7 +116,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t p_ph = 0;
     bool p_open = false;
     auto produce = [&](int budget) {
-        const uint64_t pol = policy_evict_normal();
+        // L2 policy: the raster walks group_m M-tiles down while sweeping N, so an A slab is
+        // re-read by every wave of its group (keep it: evict_last) while a B slab is dead once
+        // the current wave has passed (stream it: evict_first).  map.l2hint = 0 disables.
+        const uint64_t pol_a = map.l2hint ? policy_evict_last() : policy_evict_normal();
+        const uint64_t pol_b = map.l2hint ? policy_evict_first() : policy_evict_normal();
         while (p_t < num_tiles && budget != 0) {
             if (!p_open) {
                 int tm, tn, ks;
@@ -137,20 +142,20 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             uint8_t* sb = smem + STAGES * S::A_BYTES + p_s * S::B_BYTES;
             if constexpr (CG == 1) {
                 mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
-                tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol);
-                tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol);
+                tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
+                tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
             } else {
                 // both CTAs' bytes land on the leader's full barrier; the leader arms it
                 if (rank == 0) mbar_arrive_expect_tx(&full[p_s], 2 * S::STAGE_BYTES);
                 if constexpr (MC == 1) {
-                    tma_load_2d_cg2(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol);
+                    tma_load_2d_cg2(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
                 } else {
                     // this CTA's half of the shared A slab, to itself and its counterpart
                     const uint16_t mask = static_cast<uint16_t>((1u << rank) | (1u << (rank + CG)));
                     tma_load_2d_cg2_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[p_s], p_kb * tc::BK,
-                                       p_row_a + static_cast<int>(pair) * (tc::BM / 2), mask, pol);
+                                       p_row_a + static_cast<int>(pair) * (tc::BM / 2), mask, pol_a);
                 }
-                tma_load_2d_cg2(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol);
+                tma_load_2d_cg2(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
             }
             ++p_kb;
             if (++p_s == STAGES) { p_s = 0; p_ph ^= 1; }
