@@ -28,13 +28,19 @@ def dev_gemm(a, b, mode, kernel="auto", lda=None, ldb=None, ldc=None):
     db = torch.zeros((n, ldb), dtype=torch.int8, device="cuda")
     da[:, :k] = torch.from_numpy(a)
     db[:, :k] = torch.from_numpy(b)
-    dc = torch.full((m, ldc), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+    # C lives inside a canary frame: 8 sentinel rows before and after, and sentinel padding
+    # columns when ldc > n — any store outside the logical [m x n] block is caught (the pool's
+    # compute-sanitizer is closed, so out-of-bounds writes are checked this way)
+    frame = torch.full((m + 16, ldc), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+    dc = frame[8:8 + m]
     L = _lib.load()
     st = torch.cuda.current_stream().cuda_stream
     _lib.check(L.ngemm_cuda_gemm_u8i8_ex(da.data_ptr(), lda, db.data_ptr(), ldb, dc.data_ptr(), ldc, m, n, k, mode,
                                          KERNELS[kernel], st))
     torch.cuda.synchronize()
-    out = dc.cpu().numpy()
+    full = frame.cpu().numpy()
+    assert (full[:8] == 0x5A5A5A5A).all() and (full[8 + m:] == 0x5A5A5A5A).all(), "kernel wrote outside C's rows"
+    out = full[8:8 + m]
     if ldc > n:
         assert (out[:, n:] == 0x5A5A5A5A).all(), "kernel wrote outside C's logical columns"
     return out[:, :n]
