@@ -88,6 +88,17 @@ ngemm_status ngemm_cuda_gemm_u8i8(const uint8_t* a, int64_t lda, const int8_t* b
                                   int32_t* c, int64_t ldc, int64_t m, int64_t n, int64_t k,
                                   int sat_mode, void* stream);
 
+/* A strided batch of `batch` independent GEMMs of one shape: operand z of A / B / C starts at
+ * a + z*stride_a, b + z*stride_b, c + z*stride_c (element strides; 0 on A or B broadcasts that
+ * operand; C slices must not overlap).  The reference has no batched entry — its callers loop
+ * over gemm_conventional (gemm.hpp:327-369) once per request; for the skinny (M <= 16)
+ * serving shapes this issues one launch for the whole batch instead. */
+ngemm_status ngemm_cuda_gemm_u8i8_strided_batched(const uint8_t* a, int64_t lda, int64_t stride_a,
+                                                  const int8_t* b, int64_t ldb, int64_t stride_b,
+                                                  int32_t* c, int64_t ldc, int64_t stride_c,
+                                                  int64_t batch, int64_t m, int64_t n, int64_t k,
+                                                  int sat_mode, void* stream);
+
 /* Same, forcing one kernel (tests / bench / ncu evidence per kernel choice). */
 ngemm_status ngemm_cuda_gemm_u8i8_ex(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
                                      int32_t* c, int64_t ldc, int64_t m, int64_t n, int64_t k,

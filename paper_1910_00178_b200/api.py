@@ -257,6 +257,36 @@ def gemm_device(a, b, c=None, mode: SatMode = SatMode.WIDENING_EXACT, kernel: in
     return c
 
 
+def gemm_device_batched(a, b, c=None, mode: SatMode = SatMode.WIDENING_EXACT, stream=None):
+    """C[z] = A[z] * B[z]^T for a batch of GEMMs of one shape, on CUDA torch tensors.
+
+    A: uint8 [G, M, K] (or [M, K], broadcast), B: int8 [G, N, K] (or [N, K]), C: int32 [G, M, N].
+    Skinny shapes (M <= 16) run as one launch over the whole batch (ngemm_cuda_gemm_u8i8_strided_batched).
+    """
+    import torch
+    if a.dtype != torch.uint8 or b.dtype != torch.int8:
+        raise UnsupportedError(f"gemm: no kernel path for {a.dtype} x {b.dtype}")
+    if a.dim() not in (2, 3) or b.dim() not in (2, 3) or a.shape[-1] != b.shape[-1]:
+        raise ShapeError(f"batched gemm: A is {tuple(a.shape)}, B is {tuple(b.shape)}")
+    if a.stride(-1) != 1 or b.stride(-1) != 1:
+        raise ShapeError("gemm: operands must be K-contiguous")
+    g = a.shape[0] if a.dim() == 3 else (b.shape[0] if b.dim() == 3 else 1)
+    if (a.dim() == 3 and a.shape[0] != g) or (b.dim() == 3 and b.shape[0] != g):
+        raise ShapeError("batched gemm: batch sizes of A and B differ")
+    m, k = a.shape[-2], a.shape[-1]
+    n = b.shape[-2]
+    sa = a.stride(0) if a.dim() == 3 else 0
+    sb = b.stride(0) if b.dim() == 3 else 0
+    if c is None:
+        c = torch.empty((g, m, n), dtype=torch.int32, device=a.device)
+    if c.dtype != torch.int32 or tuple(c.shape) != (g, m, n) or c.stride(2) != 1:
+        raise ShapeError("batched gemm: C must be int32 [G, M, N] with unit column stride")
+    check(_lib.load().ngemm_cuda_gemm_u8i8_strided_batched(
+        a.data_ptr(), a.stride(-2), sa, b.data_ptr(), b.stride(-2), sb, c.data_ptr(), c.stride(1), c.stride(0),
+        g, m, n, k, int(mode), _stream_ptr(stream)))
+    return c
+
+
 class DevicePackedWeight:
     """Device-resident prepacked weight (opaque ngemm_packed_handle)."""
 

@@ -281,7 +281,8 @@ constexpr int CHUNK = 128;  // bytes of K per warp step
 __device__ __forceinline__ void mma_u8s8_m16n8k32(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                                   uint32_t a3, uint32_t b0, uint32_t b1) {
     // A operand (row-major 16x32) signed: B's rows; B operand (col-major 32x8) unsigned: A's rows.
-    asm volatile(
+    // not volatile: lets the compiler hoist the next chunk's loads above these MMAs
+    asm(
         "mma.sync.aligned.m16n8k32.row.col.s32.s8.u8.s32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, {%0,%1,%2,%3};"
         : "+r"(d[0]), "+r"(d[1]), "+r"(d[2]), "+r"(d[3])
         : "r"(a0), "r"(a1), "r"(a2), "r"(a3), "r"(b0), "r"(b1));
@@ -296,7 +297,7 @@ template <int MT, int RG, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     skinny_mma_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                       int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range,
-                      int vec_ok, int accumulate) {
+                      int vec_ok, int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc) {
     constexpr int KS = WARPS / RG;
     constexpr int NB = MT / 8;  // n8 blocks of A rows
     __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
@@ -304,6 +305,10 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int g = lane >> 2, t = lane & 3;
     pdl_launch_dependents();
     pdl_wait();
+    // strided batch: blockIdx.z selects one of several independent GEMMs of the same shape
+    A += blockIdx.z * batch_sa;
+    B += blockIdx.z * batch_sb;
+    C += blockIdx.z * batch_sc;
     const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
     const int64_t kend = min(K, kbeg + k_range);
     const int rg = warp / KS, ks = warp % KS;
@@ -317,8 +322,8 @@ __global__ void __launch_bounds__(WARPS * 32)
         const uint8_t* p = X + row * ld + k;
         if (vec_ok && k + 16 <= kend) {
             if (stream)
-                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+                asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"  // read-only for the kernel
+                    : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
             else
                 v = __ldg(reinterpret_cast<const uint4*>(p));
             return v;
@@ -406,13 +411,16 @@ template <int MT, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     skinny_sat_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                       int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range, int vec_ok,
-                      int accumulate) {
+                      int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc) {
     constexpr int V = 2 * MT;  // values per thread: rows {g, g+8} x MT
     __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     pdl_launch_dependents();
     pdl_wait();
+    A += blockIdx.z * batch_sa;  // strided batch (blockIdx.z), as in skinny_mma_kernel
+    B += blockIdx.z * batch_sb;
+    C += blockIdx.z * batch_sc;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 16;
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
     const int32_t one = (K > 0) ? 1 : 0;  // runtime 1 (keeps the adds on the FMA pipe)

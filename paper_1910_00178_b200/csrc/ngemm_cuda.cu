@@ -172,6 +172,11 @@ struct Choice {
 thread_local Choice t_force;  // the choice in effect for the launch being issued on this thread
 
 // ---------------------------------------------------------------- launchers
+// Strided batch of independent GEMMs of one shape (count 1 = a single GEMM).
+struct Batch {
+    int count = 1;
+    int64_t sa = 0, sb = 0, sc = 0;  // element strides between consecutive A / B / C
+};
 // Programmatic dependent launch: consecutive kernels on a stream overlap the next kernel's
 // launch and prologue (barrier init, TMEM alloc, descriptor prefetch) with the tail of the
 // previous one; every kernel calls griddepcontrol.wait before touching global memory, so
@@ -398,38 +403,59 @@ ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, in
 // Warp-MMA load-stream variant (skinny_mma_kernel, exact mode): 16 B-rows per row group, the
 // CTA's 8/16/32 warps split K so that ~32 warps per SM are streaming; a grid K split (atomic
 // wrap-add into a zeroed C) only when even 32 warps per row group are not enough.
-template <int MT, int WARPS>
+template <int MT, int WARPS, int RG = 1>
 ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                  int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
-                                 cudaStream_t st) {
-    const int64_t groups = (n + 15) / 16;
+                                 cudaStream_t st, const Batch& bt) {
+    const int64_t groups = (n + 16 * RG - 1) / (16 * RG);
     const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
     splits = (k + k_range - 1) / k_range;
-    if (splits > 1) {
-        ngemm_status zs = zero_c(c, ldc, m, n, nullptr, 0, di, st);
+    for (int z = 0; z < bt.count && splits > 1; ++z) {
+        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, nullptr, 0, di, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
-                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0);
-    NG_LAUNCH(skinny_mma_kernel<MT, 1, WARPS>, dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)),
+                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0);
+    NG_LAUNCH(skinny_mma_kernel<MT, RG, WARPS>,
+              dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
               dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
-              splits > 1 ? 1 : 0);
+              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
     return NGEMM_OK;
 }
 
 template <int MT>
 ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
-                                 int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
-    const int64_t groups = (n + 15) / 16;
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
+                                 const Batch& bt = Batch()) {
+    const int64_t groups = (n + 15) / 16 * bt.count;  // CTAs of all GEMMs of the batch fill the SMs
     const int64_t chunks = (k + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
     const int64_t warps_target = static_cast<int64_t>(di.sms) * 32;
     const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (warps_target + groups - 1) / groups));
     int64_t splits = 1;
     if (const char* f = std::getenv("NGEMM_SKINNY_SPLITS")) splits = std::max(1, std::atoi(f));
-    if (ks <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
-    if (ks <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
+    // Row groups per CTA (RG, 8 warps): a single skinny GEMM has too few 16-row groups to fill
+    // 148 SMs, so RG = 1 and the warps split K; a batch (or a very wide N) has CTAs to spare, so
+    // each CTA takes RG groups and its warps stream longer K runs — fewer CTA launches and K
+    // reductions per byte.  Measured on B200 (profiles/batched_skinny_r1.log): M > 8 wants the
+    // largest RG that still leaves >= 4 CTAs per SM; M <= 8 wants ~128 KB of B per CTA.
+    int rg = 1;
+    {
+        const int64_t row_groups = (n + 15) / 16 * bt.count;
+        const int64_t min_ctas = 4 * static_cast<int64_t>(di.sms);
+        for (int r : {2, 4, 8}) {
+            if (row_groups / r < min_ctas) break;
+            if (m <= 8 && static_cast<int64_t>(rg) * 16 * k >= (128 << 10)) break;
+            rg = r;
+        }
+    }
+    if (const char* f = std::getenv("NGEMM_SKINNY_RG")) rg = std::atoi(f);  // experiments
+    if (rg == 2) return launch_skinny_mma_w<MT, 8, 2>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (rg == 4) return launch_skinny_mma_w<MT, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (rg == 8) return launch_skinny_mma_w<MT, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (ks <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (ks <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
     if (ks > 32 && splits == 1) splits = (ks + 31) / 32;
-    return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st);
+    return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
 }
 
 // Saturating load-stream variant (skinny_sat_kernel): 16 B-rows per CTA, 8/16/32 warps split
@@ -438,34 +464,36 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
 template <int MT, int WARPS>
 ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                  int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const Batch& bt) {
     const int64_t groups = (n + 15) / 16;
     const int64_t k_range = round_up((k + splits - 1) / splits, 128);
     splits = (k + k_range - 1) / k_range;
-    if (splits > 1) {
-        ngemm_status zs = zero_c(c, ldc, m, n, nullptr, 0, di, st);
+    for (int z = 0; z < bt.count && splits > 1; ++z) {
+        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, nullptr, 0, di, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
-                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0);
-    NG_LAUNCH(skinny_sat_kernel<MT, WARPS>, dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits)),
+                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0);
+    NG_LAUNCH(skinny_sat_kernel<MT, WARPS>,
+              dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
               dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
-              splits > 1 ? 1 : 0);
+              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
     return NGEMM_OK;
 }
 
 template <int MT>
 ngemm_status launch_skinny_sat_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
-                                 int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
-    const int64_t groups = (n + 15) / 16;
+                                 int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
+                                 const Batch& bt = Batch()) {
+    const int64_t groups = (n + 15) / 16 * bt.count;
     const int64_t chunks = (k + 127) / 128;
     const int64_t want = static_cast<int64_t>(di.sms) * (MT >= 8 ? 16 : 32);  // resident warps to fill
     const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + groups - 1) / groups));
     constexpr int WMAX = MT >= 8 ? 16 : 32;  // 1024-thread CTAs cap registers at 64: spills for MT >= 8
-    if (ks <= 8) return launch_skinny_sat_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, 1, di, st);
+    if (ks <= 8) return launch_skinny_sat_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, 1, di, st, bt);
     if (ks <= 16 || WMAX == 16)
-        return launch_skinny_sat_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 15) / 16, di, st);
-    return launch_skinny_sat_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 31) / 32, di, st);
+        return launch_skinny_sat_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 15) / 16, di, st, bt);
+    return launch_skinny_sat_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 31) / 32, di, st, bt);
 }
 
 // Lanes-own-rows variant (skinny_rows_kernel): 32-row tiles of B x K splits.
@@ -781,6 +809,47 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
     }
 }
 
+// Strided batch: `count` independent GEMMs of one shape, operand z at base + z * stride.
+// Skinny shapes (M <= 16) run as ONE launch whose grid.z walks the batch, so the CTAs of every
+// GEMM fill the 148 SMs together and the launch latency is paid once (a single M <= 16 GEMM
+// leaves most SMs idle and is latency-bound, profiles/floor_probe_r1.log); other shapes are
+// issued back to back on the stream (each already fills the machine).  Strides of 0 on A or B
+// broadcast one operand to the whole batch; C slices must not overlap.
+ngemm_status run_gemm_batched(const uint8_t* a, int64_t lda, int64_t sa, const int8_t* b, int64_t ldb, int64_t sb,
+                              int32_t* c, int64_t ldc, int64_t sc, int64_t count, int64_t m, int64_t n, int64_t k,
+                              int mode, cudaStream_t st) {
+    if (count < 0 || count > 65535) return fail(NGEMM_ERR_SHAPE, "batched: count must be in [0, 65535]");
+    if (count == 0) return NGEMM_OK;
+    ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, mode);
+    if (s != NGEMM_OK) return s;
+    if (sa < 0 || sb < 0 || sc < 0) return fail(NGEMM_ERR_SHAPE, "batched: strides must be >= 0");
+    if ((sa != 0 && sa < (m - 1) * lda + k) || (sb != 0 && sb < (n - 1) * ldb + k))
+        return fail(NGEMM_ERR_SHAPE, "batched: a non-zero operand stride is smaller than one operand");
+    if (count > 1 && sc < (m - 1) * ldc + n) return fail(NGEMM_ERR_SHAPE, "batched: C slices overlap");
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    Choice ch;
+    const bool tuned = tuned_lookup(m, n, k, mode, &ch);
+    const int kernel = tuned ? ch.kernel : pick(m, n, k, mode);
+    if (count > 1 && kernel == NGEMM_KERNEL_SKINNY && m <= kSkinnyMaxM && k <= INT32_MAX) {
+        const Batch bt{static_cast<int>(count), sa, sb, sc};
+        if (mode == NGEMM_SAT_EXACT)
+            return m <= 8 ? launch_skinny_mma_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt)
+                          : launch_skinny_mma_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+        if (m <= 1) return launch_skinny_sat_t<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+        if (m <= 4) return launch_skinny_sat_t<4>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+        if (m <= 8) return launch_skinny_sat_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+        return launch_skinny_sat_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+    }
+    for (int64_t z = 0; z < count; ++z) {
+        s = run_gemm(a + z * sa, lda, b + z * sb, ldb, c + z * sc, ldc, m, n, k, mode, NGEMM_KERNEL_AUTO, st);
+        if (s != NGEMM_OK) return s;
+    }
+    return NGEMM_OK;
+}
+
 // ---------------------------------------------------------------- packed weights
 ngemm_status validate_meta(const ngemm_packed_meta* p) {
     if (!p) return fail(NGEMM_ERR_CONFIG, "null packed metadata");
@@ -1037,6 +1106,14 @@ int ngemm_cuda_pick_kernel(int64_t m, int64_t n, int64_t k, int sat_mode) { retu
 ngemm_status ngemm_cuda_gemm_u8i8(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                   int64_t ldc, int64_t m, int64_t n, int64_t k, int sat_mode, void* stream) {
     return run_gemm(a, lda, b, ldb, c, ldc, m, n, k, sat_mode, NGEMM_KERNEL_AUTO, static_cast<cudaStream_t>(stream));
+}
+
+ngemm_status ngemm_cuda_gemm_u8i8_strided_batched(const uint8_t* a, int64_t lda, int64_t stride_a, const int8_t* b,
+                                                  int64_t ldb, int64_t stride_b, int32_t* c, int64_t ldc,
+                                                  int64_t stride_c, int64_t batch, int64_t m, int64_t n, int64_t k,
+                                                  int sat_mode, void* stream) {
+    return run_gemm_batched(a, lda, stride_a, b, ldb, stride_b, c, ldc, stride_c, batch, m, n, k, sat_mode,
+                            static_cast<cudaStream_t>(stream));
 }
 
 ngemm_status ngemm_cuda_gemm_u8i8_ex(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,

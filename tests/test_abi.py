@@ -72,6 +72,12 @@ def test_validation_precedes_device_use():
     assert L.ngemm_cuda_gemm_u8i8(buf, 4, buf, 4, buf, 4, 0, 4, 4, 1, None) == _lib.ERR_SHAPE
     assert L.ngemm_cuda_gemm_u8i8(buf, 3, buf, 4, buf, 4, 4, 4, 4, 1, None) == _lib.ERR_SHAPE
     assert L.ngemm_cuda_gemm_u8i8(buf, 4, buf, 4, buf, 4, 4, 4, 4, 7, None) == _lib.ERR_CONFIG
+    # strided batch: C slices may not overlap, operand strides must cover one operand
+    B = L.ngemm_cuda_gemm_u8i8_strided_batched
+    assert B(buf, 4, 16, buf, 4, 16, buf, 4, 15, 2, 4, 4, 4, 1, None) == _lib.ERR_SHAPE
+    assert B(buf, 4, 8, buf, 4, 16, buf, 4, 16, 2, 4, 4, 4, 1, None) == _lib.ERR_SHAPE
+    assert B(buf, 4, 16, buf, 4, 16, buf, 4, 16, -1, 4, 4, 4, 1, None) == _lib.ERR_SHAPE
+    assert B(buf, 4, 16, buf, 4, 16, buf, 4, 16, 0, 4, 4, 4, 1, None) == _lib.OK  # empty batch: no-op
 
 
 def test_api_engine_and_kind_errors():

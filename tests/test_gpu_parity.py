@@ -393,3 +393,51 @@ def test_autotuner_picks_verified_config_and_dispatch_stays_exact(cuda, oracle, 
     api.tune_clear()
     assert api.tune_store_load(str(path)) == 4
     api.tune_clear()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("m,n,k", [(1, 768, 768), (4, 1000, 333), (16, 4096, 1024), (9, 257, 4096), (64, 300, 200)])
+def test_strided_batched(cuda, oracle, m, n, k):
+    """ngemm_cuda_gemm_u8i8_strided_batched: every batch member equals its own reference GEMM;
+    padded strides between members and between C slices are never written."""
+    import torch
+    g = 5
+    lda, ldb, ldc = k + 16, k + 32, n + 8
+    sa, sb, sc = m * lda + 48, n * ldb + 16, m * ldc + 40
+    rng = np.random.default_rng(m * 7 + n)
+    a = rng.integers(0, 256, size=g * sa, dtype=np.uint8)
+    b = rng.integers(-128, 128, size=g * sb, dtype=np.int8)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    L = _lib.load()
+    for mode in (0, 1):
+        dc = torch.full((g * sc,), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+        _lib.check(L.ngemm_cuda_gemm_u8i8_strided_batched(da.data_ptr(), lda, sa, db.data_ptr(), ldb, sb,
+                                                          dc.data_ptr(), ldc, sc, g, m, n, k, mode,
+                                                          torch.cuda.current_stream().cuda_stream))
+        torch.cuda.synchronize()
+        c = dc.cpu().numpy()
+        written = np.zeros(g * sc, bool)
+        for z in range(g):
+            az = a[z * sa: z * sa + m * lda].reshape(m, lda)[:, :k]
+            bz = b[z * sb: z * sb + n * ldb].reshape(n, ldb)[:, :k]
+            cz = c[z * sc: z * sc + m * ldc].reshape(m, ldc)[:, :n]
+            assert (cz == oracle.gemm(np.ascontiguousarray(az), np.ascontiguousarray(bz), mode)).all(), (z, mode)
+            idx = z * sc + np.arange(m)[:, None] * ldc + np.arange(n)[None, :]
+            written[idx.ravel()] = True
+        assert (c[~written] == 0x5A5A5A5A).all(), "batched kernel wrote outside a C slice"
+
+
+@pytest.mark.gpu
+def test_batched_broadcast_and_api(cuda, oracle):
+    import torch
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 256, size=(8, 4096), dtype=np.uint8)
+    b = rng.integers(-128, 128, size=(6, 1024, 4096), dtype=np.int8)
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    for mode in (api.SatMode.HARDWARE_SATURATING, api.SatMode.WIDENING_EXACT):
+        c = api.gemm_device_batched(da, db, mode=mode).cpu().numpy()  # A broadcast (stride 0)
+        for z in range(6):
+            assert (c[z] == oracle.gemm(a, b[z], int(mode))).all()
+    with pytest.raises(api.ShapeError):
+        api.gemm_device_batched(torch.zeros((2, 4, 8), dtype=torch.uint8, device="cuda"),
+                                torch.zeros((3, 4, 8), dtype=torch.int8, device="cuda"))
