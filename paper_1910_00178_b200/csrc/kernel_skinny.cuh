@@ -14,6 +14,12 @@
 
 #include "ptx.cuh"
 
+// Phase-trace hooks for scripts/probes/skinny_trace.cu (no code in the library build).
+#ifndef SKINNY_TRACE_AT
+#define SKINNY_TRACE_AT(phase)
+#define SKINNY_TRACE_END()
+#endif
+
 namespace ngemm_dev {
 
 namespace skinny {
@@ -278,6 +284,32 @@ namespace skinny_mma {
 constexpr int CHUNK = 128;  // bytes of K per warp step
 }  // namespace skinny_mma
 
+// Tail of a 16-byte operand read (fewer than 16 bytes left in the K range, or an operand that
+// is not 16-byte aligned): byte loads, zero fill; a rolled loop keeps the kernels' code small.
+__device__ __forceinline__ uint4 load16_tail(const uint8_t* p, int64_t avail) {
+    uint32_t w[4] = {0, 0, 0, 0};
+#pragma unroll 1
+    for (int i = 0; i < 16 && i < avail; ++i) w[i >> 2] |= static_cast<uint32_t>(__ldg(p + i)) << (8 * (i & 3));
+    return make_uint4(w[0], w[1], w[2], w[3]);
+}
+
+// 16 bytes of an operand row at p; avail = bytes of the row left in the K range (<= 0: zero).
+// STREAM: B (read once, bypass L1); else A (re-read by every warp, via L1).
+template <bool STREAM>
+__device__ __forceinline__ uint4 load16_row(const uint8_t* p, int64_t avail, bool vec) {
+    uint4 v = make_uint4(0, 0, 0, 0);
+    if (avail <= 0) return v;
+    if (vec && avail >= 16) {
+        if constexpr (STREAM)
+            asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"  // read-only for the kernel
+                : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
+        else
+            v = __ldg(reinterpret_cast<const uint4*>(p));
+        return v;
+    }
+    return load16_tail(p, avail);
+}
+
 __device__ __forceinline__ void mma_u8s8_m16n8k32(int32_t (&d)[4], uint32_t a0, uint32_t a1, uint32_t a2,
                                                   uint32_t a3, uint32_t b0, uint32_t b1) {
     // A operand (row-major 16x32) signed: B's rows; B operand (col-major 32x8) unsigned: A's rows.
@@ -303,54 +335,58 @@ __global__ void __launch_bounds__(WARPS * 32)
     __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
+    SKINNY_TRACE_AT(0);
     pdl_launch_dependents();
-    pdl_wait();
     // strided batch: blockIdx.z selects one of several independent GEMMs of the same shape
     A += blockIdx.z * batch_sa;
     B += blockIdx.z * batch_sb;
     C += blockIdx.z * batch_sc;
     const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
     const int64_t kend = min(K, kbeg + k_range);
+    if (vec_ok & 2) {
+        // warm L2 with this CTA's B rows (and A) while the preceding grid drains: the HBM fetch
+        // overlaps its tail instead of starting after it (see prefetch_l2_bulk)
+        const uint32_t span = static_cast<uint32_t>((kend - kbeg) & ~int64_t(15));
+        const int64_t nrow = static_cast<int64_t>(blockIdx.x) * RG * 16 + tid;
+        if (span != 0) {
+            if (tid < RG * 16) {
+                if (nrow < N) prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(B) + nrow * ldb + kbeg, span);
+            } else if (tid < RG * 16 + M) {
+                prefetch_l2_bulk(A + (tid - RG * 16) * lda + kbeg, span);
+            }
+        }
+    }
+    pdl_wait();
+    SKINNY_TRACE_AT(1);
     const int rg = warp / KS, ks = warp % KS;
     const int64_t n0 = (static_cast<int64_t>(blockIdx.x) * RG + rg) * 16;
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
 
-    // 16 bytes of row `row` of X at byte k (zero outside rows/K); streaming or L1-cached
-    auto load16 = [&](const uint8_t* X, int64_t ld, int64_t rows, int64_t row, int64_t k, bool stream) -> uint4 {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (row >= rows || k >= kend) return v;
-        const uint8_t* p = X + row * ld + k;
-        if (vec_ok && k + 16 <= kend) {
-            if (stream)
-                asm("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"  // read-only for the kernel
-                    : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-            else
-                v = __ldg(reinterpret_cast<const uint4*>(p));
-            return v;
-        }
-        uint32_t w[4] = {0, 0, 0, 0};
+    // per-thread operand rows: B rows n0+g and n0+g+8, A rows nb*8+g; thread t reads bytes
+    // [c*64 + t*16, +16) of each 128-byte chunk (rows outside the matrix read as zeros)
+    const bool vec = vec_ok != 0;
+    const int64_t kt = kbeg + t * 16;
+    const int64_t rem = kend - kt;  // bytes of the K range left from this thread's first byte
+    const uint8_t* pb = Bu + (n0 + g) * ldb + kt;
+    const uint8_t* pa = A + g * lda + kt;
+    const bool ok_b0 = n0 + g < N, ok_b1 = n0 + g + 8 < N;
+    // B rows (g, g+8) x halves c; A rows (nb*8 + g) x halves c
+    auto load_chunk = [&](int64_t ch, uint4 (&bv)[2][2], uint4 (&av)[NB][2]) {
 #pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if (k + i < kend) w[i >> 2] |= static_cast<uint32_t>(__ldg(p + i)) << (8 * (i & 3));
-        return make_uint4(w[0], w[1], w[2], w[3]);
+        for (int c = 0; c < 2; ++c) {
+            const int64_t o = ch * skinny_mma::CHUNK + c * 64;
+            bv[0][c] = load16_row<true>(pb + o, ok_b0 ? rem - o : 0, vec);
+            bv[1][c] = load16_row<true>(pb + 8 * ldb + o, ok_b1 ? rem - o : 0, vec);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb)
+                av[nb][c] = load16_row<false>(pa + nb * 8 * lda + o, (nb * 8 + g < M) ? rem - o : 0, vec);
+        }
     };
 
     int32_t d[NB][4];
 #pragma unroll
     for (int j = 0; j < NB; ++j) d[j][0] = d[j][1] = d[j][2] = d[j][3] = 0;
-
-    const int64_t chunks = (kend - kbeg + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
-#pragma unroll 4
-    for (int64_t ch = ks; ch < chunks; ch += KS) {
-        const int64_t k0 = kbeg + ch * skinny_mma::CHUNK;
-        uint4 bv[2][2], av[NB][2];  // B rows (g, g+8) x halves; A rows (nb*8 + g) x halves
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            bv[0][c] = load16(Bu, ldb, N, n0 + g, k0 + c * 64 + t * 16, true);
-            bv[1][c] = load16(Bu, ldb, N, n0 + g + 8, k0 + c * 64 + t * 16, true);
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) av[nb][c] = load16(A, lda, M, nb * 8 + g, k0 + c * 64 + t * 16, false);
-        }
+    auto compute = [&](const uint4 (&bv)[2][2], const uint4 (&av)[NB][2]) {
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
             const uint32_t ba[4] = {bv[0][c].x, bv[0][c].y, bv[0][c].z, bv[0][c].w};
@@ -364,8 +400,17 @@ __global__ void __launch_bounds__(WARPS * 32)
                                       aa[2 * j + 1]);
             }
         }
+    };
+
+    const int64_t chunks = (kend - kbeg + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
+#pragma unroll 4
+    for (int64_t ch = ks; ch < chunks; ch += KS) {
+        uint4 bv[2][2], av[NB][2];
+        load_chunk(ch, bv, av);
+        compute(bv, av);
     }
 
+    SKINNY_TRACE_AT(2);
     // meet the KS warps of this row group in smem: red[rg][ks][16 rows][MT cols]
 #pragma unroll
     for (int nb = 0; nb < NB; ++nb) {
@@ -378,6 +423,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         r8[1] = d[nb][3];
     }
     __syncthreads();
+    SKINNY_TRACE_AT(3);
     for (int i = tid; i < RG * 16 * MT; i += WARPS * 32) {
         const int m = i / (RG * 16), rr = i % (RG * 16);  // consecutive threads -> consecutive n
         const int r_g = rr / 16, row = rr % 16;
@@ -391,6 +437,8 @@ __global__ void __launch_bounds__(WARPS * 32)
             else *dst = static_cast<int32_t>(s);
         }
     }
+    SKINNY_TRACE_AT(4);
+    SKINNY_TRACE_END();
 }
 
 }  // namespace ngemm_dev
@@ -417,11 +465,22 @@ __global__ void __launch_bounds__(WARPS * 32)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     pdl_launch_dependents();
-    pdl_wait();
     A += blockIdx.z * batch_sa;  // strided batch (blockIdx.z), as in skinny_mma_kernel
     B += blockIdx.z * batch_sb;
     C += blockIdx.z * batch_sc;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 16;
+    if (vec_ok & 2) {  // warm L2 before the dependency wait, as in skinny_mma_kernel
+        const int64_t kb = static_cast<int64_t>(blockIdx.y) * k_range;
+        const uint32_t span = static_cast<uint32_t>((min(K, kb + k_range) - kb) & ~int64_t(15));
+        if (span != 0 && kb < K) {
+            if (tid < 16) {
+                if (n0 + tid < N) prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(B) + (n0 + tid) * ldb + kb, span);
+            } else if (tid < 16 + M) {
+                prefetch_l2_bulk(A + (tid - 16) * lda + kb, span);
+            }
+        }
+    }
+    pdl_wait();
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
     const int32_t one = (K > 0) ? 1 : 0;  // runtime 1 (keeps the adds on the FMA pipe)
 

@@ -56,6 +56,7 @@ struct TileMap {
     int group_m;                   // rasterisation: group_m M-tiles walked down before moving along N
     int preissue;                  // 1-CTA tiles: issue the first STAGES loads before the block sync
     int l2hint;                    // L2 eviction hints: A evict_last, B evict_first
+    int prefetch;                  // warm L2 with the first operand slabs before the PDL wait
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -167,6 +168,21 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
         if (c_mode != 2) tma_prefetch(&tma_c);
+        if (MC == 1 && map.prefetch && guard == nullptr && unit < num_tiles) {
+            // warm L2 with this CTA's first STAGES operand slabs before the dependency wait
+            // (tma_prefetch_tile_2d: prefetch only, re-read after pdl_wait), so the first HBM
+            // round trips overlap the preceding grid's tail and this CTA's setup
+            int tm, tn, ks;
+            map.coords(unit, tm, tn, ks);
+            const int kb0 = ks * kb_per_split;
+            const int kb1 = min(num_kb_total, min(kb0 + kb_per_split, kb0 + STAGES));
+            const int row_a = tm * UMMA_M + static_cast<int>(rank) * tc::BM;
+            const int row_b = tn * BN + static_cast<int>(rank) * (BN / CG);
+            for (int kb = kb0; kb < kb1; ++kb) {
+                tma_prefetch_tile_2d(&tma_a, kb * tc::BK, row_a);
+                tma_prefetch_tile_2d(&tma_b, kb * tc::BK, row_b);
+            }
+        }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], MC);  // one commit per pair that reads this stage

@@ -403,6 +403,22 @@ ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, in
 // Warp-MMA load-stream variant (skinny_mma_kernel, exact mode): 16 B-rows per row group, the
 // CTA's 8/16/32 warps split K so that ~32 warps per SM are streaming; a grid K split (atomic
 // wrap-add into a zeroed C) only when even 32 warps per row group are not enough.
+// Skinny kernels' `vec_ok` argument: bit 0 = operands allow 16-byte vector loads, bit 1 = also
+// warm L2 with the CTA's operand rows before the PDL dependency wait (NGEMM_L2_PREFETCH=0 off).
+bool l2_prefetch_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("NGEMM_L2_PREFETCH");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+
+int skinny_vec_flags(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, const Batch& bt) {
+    const bool vec = reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
+                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0;
+    return vec ? (l2_prefetch_enabled() ? 3 : 1) : 0;
+}
+
 template <int MT, int WARPS, int RG = 1>
 ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                  int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
@@ -414,8 +430,7 @@ ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b,
         ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, nullptr, 0, di, st);
         if (zs != NGEMM_OK) return zs;
     }
-    const int vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
-                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0);
+    const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
     NG_LAUNCH(skinny_mma_kernel<MT, RG, WARPS>,
               dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
               dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
@@ -472,8 +487,7 @@ ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b,
         ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, nullptr, 0, di, st);
         if (zs != NGEMM_OK) return zs;
     }
-    const int vec = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
-                     reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0);
+    const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
     NG_LAUNCH(skinny_sat_kernel<MT, WARPS>,
               dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
               dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
@@ -668,6 +682,7 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     if (const char* e = std::getenv("NGEMM_TC_PREISSUE")) map.preissue = std::atoi(e);  // experiments
     map.l2hint = 1;
     if (const char* e = std::getenv("NGEMM_TC_L2HINT")) map.l2hint = std::atoi(e);  // experiments
+    map.prefetch = l2_prefetch_enabled() ? 1 : 0;
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
     if (map.splits > 1) {
         c_mode = 1;

@@ -162,6 +162,20 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
 // Wait until the preceding grid in the stream has completed and its memory is visible (no-op
 // when the kernel was not launched with programmatic stream serialization).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// Warm L2 with global bytes [p, p + bytes) (p 16-byte aligned, bytes a multiple of 16).  Safe to
+// issue BEFORE pdl_wait(): the bytes are only warmed, never consumed — they are re-read after
+// the wait, and L2 is the device's point of coherence, so a line the preceding grid is still
+// writing is never served stale (nothing is brought into L1 early).
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+// Same for one box of a TMA tensor map at coordinates (c0, c1).
+__device__ __forceinline__ void tma_prefetch_tile_2d(const CUtensorMap* map, int32_t c0, int32_t c1) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile [%0, {%1, %2}];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(c0), "r"(c1)
+                 : "memory");
+}
 // Let the dependent grid start launching (its CTAs run their prologue, then pdl_wait()).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 

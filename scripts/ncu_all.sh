@@ -1,5 +1,6 @@
 #!/bin/bash
 # One --set full capture per kernel choice (each after its plain run exits 0), plus launch lists.
+# usage: ncu_all.sh [tag ...]   (no tags = all)
 set -u
 mkdir -p gpurun_out
 cap() {  # tag, bench args, kernel regex
@@ -11,9 +12,15 @@ cap() {  # tag, bench args, kernel regex
       python bench.py $args > gpurun_out/ncu_full_$tag.log 2>&1
   echo "captured $tag rc=$?"
 }
-cap c5_tc      "--steps 3 --warmup 2 --no-cpu --no-e2e --eager" tc_gemm
-cap c1_tc      "--steps 3 --warmup 2 --no-cpu --no-e2e --eager --shape 1024x1024x1024" tc_gemm
-cap c2_tcskinny "--steps 3 --warmup 2 --no-cpu --no-e2e --eager --shape 16x4096x1024" tc_skinny
-cap c2_rows_sat "--steps 3 --warmup 2 --no-cpu --no-e2e --eager --shape 16x4096x1024 --mode sat" skinny_rows
-cap c4_simt_sat "--steps 3 --warmup 2 --no-cpu --no-e2e --eager --shape 2048x2048x2048 --mode sat" simt_gemm
-cap c3_tc      "--steps 3 --warmup 2 --no-cpu --no-e2e --eager --shape 2048x4096x1024" tc_gemm
+want() { [ $# -eq 0 ] && return 0; for t in "${TAGS[@]}"; do [ "$t" = "$1" ] && return 0; done; return 1; }
+TAGS=("$@")
+E="--steps 3 --warmup 2 --no-cpu --no-e2e --eager"
+want c5_tc        && cap c5_tc        "$E" tc_gemm
+want c1_tc        && cap c1_tc        "$E --shape 1024x1024x1024" tc_gemm
+want c2_mma       && cap c2_mma       "$E --shape 16x4096x1024" skinny_mma
+want c2_mma_m1    && cap c2_mma_m1    "$E --shape 1x4096x1024" skinny_mma
+want c2_sat       && cap c2_sat       "$E --shape 16x4096x1024 --mode sat" skinny_sat
+want c2_tcskinny  && NGEMM_SKINNY_VARIANT=2 cap c2_tcskinny "$E --shape 16x4096x1024" tc_skinny
+want c2_rows_sat  && cap c2_rows_sat  "$E --shape 16x768x768 --mode sat" skinny_rows
+want c4_simt_sat  && cap c4_simt_sat  "$E --shape 2048x2048x2048 --mode sat" simt_gemm
+want c3_tc        && cap c3_tc        "$E --shape 2048x4096x1024" tc_gemm

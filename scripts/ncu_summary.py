@@ -61,10 +61,16 @@ def main():
         by[name][1] += t
     summ["launch_list"] = {"total_ns": tot, "kernels": {k: {"launches": n, "ns": t, "share": round(t / tot, 4) if tot else None}
                                                        for k, (n, t) in sorted(by.items(), key=lambda x: -x[1][1])}}
-    os.makedirs(os.path.join(ROOT, "profiles"), exist_ok=True)
-    out = os.path.join(ROOT, "profiles", f"ncu_{tag}.json")
+    out_dir = os.environ.get("NCU_OUT", os.path.join(ROOT, "profiles"))  # gpurun_out when run on the box
+    os.makedirs(out_dir, exist_ok=True)
+    out = os.path.join(out_dir, f"ncu_{tag}.json")
     json.dump(summ, open(out, "w"), indent=1)
     print(json.dumps(summ, indent=1)[:4000])
+    if os.path.exists(rep) and os.environ.get("NCU_SOURCE"):
+        # per-line source view (SASS + CUDA correlation) of the captured kernel, for stall analysis
+        src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                             capture_output=True, text=True).stdout
+        open(os.path.join(out_dir, f"source_{tag}.csv"), "w").write(src)
 
 
 if __name__ == "__main__":
