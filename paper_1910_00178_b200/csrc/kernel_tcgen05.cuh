@@ -55,7 +55,7 @@ struct TileMap {
     int tiles_m, tiles_n, splits;  // tiles_m counts 128*CG-row tiles
     int group_m;                   // rasterisation: group_m M-tiles walked down before moving along N
     int preissue;                  // 1-CTA tiles: issue the first STAGES loads before the block sync
-    int l2hint;                    // L2 eviction hints: A evict_last, B evict_first
+    int l2hint;                    // L2 eviction hints: bit 0 A evict_last, bit 1 B evict_first
     int prefetch;                  // warm L2 with the first operand slabs before the PDL wait
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
@@ -119,9 +119,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     auto produce = [&](int budget) {
         // L2 policy: the raster walks group_m M-tiles down while sweeping N, so an A slab is
         // re-read by every wave of its group (keep it: evict_last) while a B slab is dead once
-        // the current wave has passed (stream it: evict_first).  map.l2hint = 0 disables.
-        const uint64_t pol_a = map.l2hint ? policy_evict_last() : policy_evict_normal();
-        const uint64_t pol_b = map.l2hint ? policy_evict_first() : policy_evict_normal();
+        // the current wave has passed (stream it: evict_first).  map.l2hint bits select each.
+        const uint64_t pol_a = (map.l2hint & 1) ? policy_evict_last() : policy_evict_normal();
+        const uint64_t pol_b = (map.l2hint & 2) ? policy_evict_first() : policy_evict_normal();
         while (p_t < num_tiles && budget != 0) {
             if (!p_open) {
                 int tm, tn, ks;

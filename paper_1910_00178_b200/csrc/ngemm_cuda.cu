@@ -680,7 +680,7 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     // pre-issuing the first loads before the block sync measured slower (profiles/ab_preissue_r1.log)
     map.preissue = 0;
     if (const char* e = std::getenv("NGEMM_TC_PREISSUE")) map.preissue = std::atoi(e);  // experiments
-    map.l2hint = 1;
+    map.l2hint = 3;
     if (const char* e = std::getenv("NGEMM_TC_L2HINT")) map.l2hint = std::atoi(e);  // experiments
     map.prefetch = l2_prefetch_enabled() ? 1 : 0;
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
