@@ -24,6 +24,12 @@ $(LIB): $(wildcard $(CSRC)/*.cu $(CSRC)/*.cuh) include/ngemm_cuda.h
 oracle:
 	$(MAKE) -s -C oracle
 
+# phase-trace build of the library (scripts/probes/tc_trace.py); never loaded by the package
+trace: $(PKG)/lib/libngemm_cuda_trace.so
+$(PKG)/lib/libngemm_cuda_trace.so: $(wildcard $(CSRC)/*.cu $(CSRC)/*.cuh) include/ngemm_cuda.h
+	mkdir -p $(PKG)/lib
+	$(NVCC) $(NVFLAGS) -DNGEMM_TRACE -o $@ $(CSRC)/ngemm_cuda.cu
+
 ptxas:
 	$(NVCC) $(NVFLAGS) -Xptxas -v -o /tmp/ngemm_ptxas.so $(CSRC)/ngemm_cuda.cu 2>&1 | grep -E "Function properties|registers|spill|Compiling entry" | head -80
 
@@ -34,4 +40,4 @@ clean:
 	rm -f $(LIB) $(CLI)
 	$(MAKE) -s -C oracle clean
 
-.PHONY: all oracle ptxas sass clean
+.PHONY: all oracle trace ptxas sass clean

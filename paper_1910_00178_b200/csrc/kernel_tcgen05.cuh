@@ -25,6 +25,14 @@
 
 #include "ptx.cuh"
 
+// Phase-trace hooks (scripts/probes/tc_trace.py; the library build compiles them out).
+#ifndef TC_TRACE_NOW
+#define TC_TRACE_NOW(p)
+#define TC_TRACE_KEEP(p)
+#define TC_TRACE_FLUSH()
+#define TC_TRACE_END()
+#endif
+
 namespace ngemm_dev {
 
 namespace tc {
@@ -57,6 +65,9 @@ struct TileMap {
     int preissue;                  // 1-CTA tiles: issue the first STAGES loads before the block sync
     int l2hint;                    // L2 eviction hints: bit 0 A evict_last, bit 1 B evict_first
     int prefetch;                  // warm L2 with the first operand slabs before the PDL wait
+    int dbg;                       // probes only (NGEMM_TC_DBG): bit 0 skip C stores, bit 1 skip MMAs,
+                                   // bit 2 skip operand loads (1-CTA configs)
+    int trace_id;                  // trace build: launch index for the phase stamps (-1 otherwise)
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -87,6 +98,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         pdl_wait();
         if (!sat_safe(guard)) return;  // uniform across the grid (and across a CTA pair)
     }
+    TC_TRACE_KEEP(0);
     using S = tc::Smem<BN, STAGES, CG>;
     constexpr int UMMA_M = tc::BM * CG;
     extern __shared__ uint8_t smem_raw[];
@@ -141,7 +153,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             mbar_wait(&empty[p_s], p_ph ^ 1);  // returns at once for the first STAGES fills
             uint8_t* sa = smem + p_s * S::A_BYTES;
             uint8_t* sb = smem + STAGES * S::A_BYTES + p_s * S::B_BYTES;
-            if constexpr (CG == 1) {
+            if (CG == 1 && (map.dbg & 4)) {
+                mbar_arrive(&full[p_s]);  // probes only: no operand traffic
+            } else if constexpr (CG == 1) {
                 mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
                 tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
                 tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
@@ -204,10 +218,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if constexpr (CL > 1) cluster_sync(); else __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
+    TC_TRACE_KEEP(1);
     pdl_wait();  // operands / C may belong to the preceding kernel in the stream
+    TC_TRACE_FLUSH();
 
     if (warp == 0) {
-        if (lane == 0) produce(-1);
+        if (lane == 0) {
+            TC_TRACE_NOW(3);
+            produce(-1);
+            TC_TRACE_NOW(4);
+        }
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (single thread of the leader CTA)
@@ -227,10 +247,12 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 for (int kb = kb0; kb < kb1; ++kb) {
                     mbar_wait(&full[s], ph);
                     tc_fence_after();
+                    if (t == unit && kb == kb0) TC_TRACE_NOW(5);
                     const uint32_t sa = smem_u32(smem + s * S::A_BYTES);
                     const uint32_t sb = smem_u32(smem + STAGES * S::A_BYTES + s * S::B_BYTES);
 #pragma unroll
                     for (int k = 0; k < tc::BK / tc::UMMA_K; ++k) {
+                        if (map.dbg & 2) break;
                         mma_i8<CG>(d_tmem, sdesc_k_sw128(sa + k * tc::UMMA_K), sdesc_k_sw128(sb + k * tc::UMMA_K),
                                    idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     }
@@ -243,6 +265,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 acc ^= 1;
                 if (acc == 0) acc_ph ^= 1;
             }
+            TC_TRACE_NOW(6);
         }
     } else if (warp >= 4) {
         // ---------------- epilogue (both CTAs): TMEM -> registers -> swizzled smem -> TMA store
@@ -258,6 +281,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const bool has_k = kb0 < num_kb_total;
             mbar_wait(&tfull[acc], acc_ph);
             tc_fence_after();
+            if (t == unit && warp == 4 && lane == 0) TC_TRACE_NOW(7);
             const int row0 = tm * UMMA_M + static_cast<int>(rank) * tc::BM + ew * 32;
             const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
 #pragma unroll 1
@@ -279,7 +303,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                                      v[4 * j + 3]);
                     fence_proxy_async_smem();
                     __syncwarp();
-                    if (lane == 0) {
+                    if (lane == 0 && !(map.dbg & 1)) {
                         if (c_mode == 0) tma_store_2d(&tma_c, buf, col0, row0);
                         else tma_reduce_add_2d(&tma_c, buf, col0, row0);
                         tma_store_commit();
@@ -304,7 +328,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             acc ^= 1;
             if (acc == 0) acc_ph ^= 1;
         }
-        if (lane == 0) tma_store_wait<0>();
+        // the staging smem must be read out before the CTA exits; the global writes themselves
+        // complete before the grid does (and before a dependent grid's griddepcontrol.wait)
+        if (lane == 0) tma_store_wait_read<0>();
+        if (warp == 4 && lane == 0) TC_TRACE_NOW(8);
     }
 
     tc_fence_before();
@@ -313,6 +340,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         tc_fence_after();
         tmem_dealloc<CG>(tmem_base, S::TMEM_COLS);
     }
+    TC_TRACE_END();
 }
 
 }  // namespace ngemm_dev

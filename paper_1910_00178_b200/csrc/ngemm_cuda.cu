@@ -24,6 +24,34 @@
 #include <utility>
 #include <vector>
 
+#ifdef NGEMM_TRACE
+// Trace build only (make trace -> libngemm_cuda_trace.so, scripts/probes/tc_trace.py): per
+// launch and CTA, %globaltimer stamps of the tcgen05 kernel's phases.  The launch index comes
+// from the host (TileMap::trace_id, one per captured launch), so recording a stamp is a single
+// global store: no loads or atomics that would stall the traced thread.
+constexpr int kTraceL = 64, kTraceCta = 160, kTraceP = 10;
+__device__ unsigned long long g_tc_trace[kTraceL][kTraceCta][kTraceP];
+int g_trace_next = 0;  // host: id of the next traced launch
+__device__ __forceinline__ unsigned long long trace_now() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void trace_put(int L, int p, unsigned long long t) {
+    if (L >= 0 && L < kTraceL && blockIdx.x < kTraceCta) g_tc_trace[L][blockIdx.x][p] = t;
+}
+#define TC_TRACE_KEEP(p) const unsigned long long _tck##p = trace_now();
+#define TC_TRACE_NOW(p) trace_put(map.trace_id, p, trace_now())
+#define TC_TRACE_FLUSH()                       \
+    if (threadIdx.x == 0) {                    \
+        trace_put(map.trace_id, 0, _tck0);     \
+        trace_put(map.trace_id, 1, _tck1);     \
+        trace_put(map.trace_id, 2, trace_now()); \
+    }
+#define TC_TRACE_END() \
+    if (threadIdx.x == 0) trace_put(map.trace_id, 9, trace_now());
+#endif
+
 #include "kernel_layout.cuh"
 #include "kernel_simt.cuh"
 #include "kernel_skinny.cuh"
@@ -226,6 +254,8 @@ cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
 template <typename K>
 ngemm_status set_smem(K kernel, int bytes) {
     NG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    // largest shared-memory carveout, so two lean CTAs (or a lean CTA and the next grid's) fit
+    NG_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     return NGEMM_OK;
 }
 
@@ -593,18 +623,29 @@ ngemm_status make_tmap_c(CUtensorMap* map, const int32_t* c, int64_t rows, int64
 }
 
 // Tile configurations of the tcgen05 kernel (per CTA: 128 rows of A; cta_group::2 pairs two SMs).
-enum TcCfg { TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_QUAD256 = 4, TC_NUM_CFG = 5 };
+enum TcCfg {
+    TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_QUAD256 = 4, TC_LEAN128 = 5, TC_LEAN64 = 6,
+    TC_NUM_CFG = 7
+};
 struct TcCfgInfo {
     int cg, bn, mc;
     double cycles_per_kb;  // MMA issue floor per 128-byte K slab, with the smem-bandwidth cap
+    int lean;              // <= ~100 KB smem and <= 256 TMEM columns: two CTAs fit on an SM
 };
 constexpr TcCfgInfo kTcCfg[TC_NUM_CFG] = {
-    {2, 256, 1, 512.0},  // 256x256x128 int8 per pair at 8192 MAC/clk/SM
-    {1, 256, 1, 520.0},  // 128x256: 96 B/clk of smem operand reads
-    {1, 128, 1, 300.0},  // 128x128: 128 B/clk, at the smem port limit
-    {1, 64, 1, 192.0},   // 128x64 : smem-bound (192 B/clk needed)
-    {2, 256, 2, 512.0},  // two pairs sharing A (multicast): 256x512 per 4-CTA cluster
+    {2, 256, 1, 512.0, 0},  // 256x256x128 int8 per pair at 8192 MAC/clk/SM
+    {1, 256, 1, 520.0, 0},  // 128x256: 96 B/clk of smem operand reads
+    {1, 128, 1, 300.0, 0},  // 128x128: 128 B/clk, at the smem port limit
+    {1, 64, 1, 192.0, 0},   // 128x64 : smem-bound (192 B/clk needed)
+    {2, 256, 2, 512.0, 0},  // two pairs sharing A (multicast): 256x512 per 4-CTA cluster
+    {1, 128, 1, 450.0, 1},  // 128x128, 2 stages: latency-limited stream, but co-resident
+    {1, 64, 1, 330.0, 1},   // 128x64, 3 stages
 };
+// A launch whose CTAs cannot share an SM with the previous grid's pays the full CTA launch +
+// barrier/TMEM setup after that grid drains (~1.5 us more per launch than a lean
+// configuration, profiles/tc_trace_r1.log); lean CTAs become resident early under PDL and do
+// their setup and L2 prefetch while the previous grid still runs.
+constexpr double kNotLeanCycles = 2800.0;
 
 struct TcPlan {
     int cfg, splits;
@@ -637,6 +678,7 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
             const int64_t waves = (work + units - 1) / units;
             const double kb = static_cast<double>((num_kb + splits - 1) / splits);
             double t = static_cast<double>(waves) * kb * ci.cycles_per_kb + 600.0 + ci.bn * 8.0;
+            if (!ci.lean) t += kNotLeanCycles;
             if (splits > 1) t += 1500.0;                 // zeroing C + reduce-add traffic
             if (ci.cg == 2) t *= 0.97;                    // less L2->SM traffic per MAC
             if (ci.mc == 2) t *= 0.98;                    // A multicast: a further 25% less
@@ -683,6 +725,12 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.l2hint = 3;
     if (const char* e = std::getenv("NGEMM_TC_L2HINT")) map.l2hint = std::atoi(e);  // experiments
     map.prefetch = l2_prefetch_enabled() ? 1 : 0;
+    map.dbg = 0;
+    map.trace_id = -1;
+#ifdef NGEMM_TRACE
+    if (const char* e = std::getenv("NGEMM_TC_DBG")) map.dbg = std::atoi(e);  // trace build only
+    map.trace_id = g_trace_next++;
+#endif
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
     if (map.splits > 1) {
         c_mode = 1;
@@ -736,6 +784,8 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
         case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
         }
     }
@@ -1453,8 +1503,8 @@ ngemm_status ngemm_cuda_tune(int64_t m, int64_t n, int64_t k, int sat_mode, int 
 
     std::vector<Choice> cands;
     if (m <= kSkinnyMaxM) {
-        for (int v = 0; v < 4; ++v) {
-            if (sat_mode != NGEMM_SAT_EXACT && v >= 2) continue;
+        for (int v = 0; v < 5; ++v) {
+            if (sat_mode == NGEMM_SAT_EXACT ? v == 4 : (v == 2 || v == 3)) continue;
             Choice c;
             c.kernel = NGEMM_KERNEL_SKINNY;
             c.skinny_variant = v;
@@ -1606,3 +1656,15 @@ ngemm_status ngemm_cuda_free(void* p) {
 }
 
 }  // extern "C"
+
+#ifdef NGEMM_TRACE
+extern "C" int ngemm_trace_reset(void) {  // zero the stamps; the next traced launch gets id 0
+    static unsigned long long zeros[kTraceL * kTraceCta * kTraceP];
+    g_trace_next = 0;
+    return cudaMemcpyToSymbol(g_tc_trace, zeros, sizeof(zeros)) == cudaSuccess ? 0 : 1;
+}
+extern "C" int ngemm_trace_read(void* dst, size_t bytes) {
+    if (bytes > sizeof(g_tc_trace)) bytes = sizeof(g_tc_trace);
+    return cudaMemcpyFromSymbol(dst, g_tc_trace, bytes) == cudaSuccess ? 0 : 1;
+}
+#endif
