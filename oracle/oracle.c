@@ -51,6 +51,14 @@ void ngo_mat_random_i8(int8_t* out, int64_t rows, int64_t cols, uint64_t seed, i
     for (int64_t i = 0; i < n; ++i) out[i] = (int8_t)ngo_rng_next_in(&r, lo, hi);
 }
 
+/* mat_random for ElemKind::I16 (matrix.hpp:146-158): same stream, value cast to int16. */
+void ngo_mat_random_i16(int16_t* out, int64_t rows, int64_t cols, uint64_t seed, int64_t lo, int64_t hi) {
+    ngo_rng r;
+    ngo_rng_seed(&r, seed);
+    int64_t n = rows * cols;
+    for (int64_t i = 0; i < n; ++i) out[i] = (int16_t)ngo_rng_next_in(&r, lo, hi);
+}
+
 /* SURVEY.md 8(d) c2 generator (ours; the reference has no normal generator). */
 void ngo_mat_normal_i8(int8_t* out, int64_t rows, int64_t cols, uint64_t seed, double sigma) {
     ngo_rng r;
@@ -90,6 +98,20 @@ void ngo_gemm_ref_rows(const uint8_t* a, int64_t lda, const int8_t* b, int64_t l
             uint32_t acc = 0;
             for (int64_t ki = 0; ki < k; ++ki) acc += (uint32_t)((int32_t)arow[ki] * brow[ki]);
             crow[ni] = (int32_t)acc;
+        }
+    }
+}
+
+/* gemm.hpp:36-52 on i16 operands: every product fits int32; sum in uint32 (wraps). */
+void ngo_gemm_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                  int64_t m, int64_t n, int64_t k) {
+    for (int64_t mi = 0; mi < m; ++mi) {
+        const int16_t* arow = a + mi * lda;
+        for (int64_t ni = 0; ni < n; ++ni) {
+            const int16_t* brow = b + ni * ldb;
+            uint32_t acc = 0;
+            for (int64_t ki = 0; ki < k; ++ki) acc += (uint32_t)((int32_t)arow[ki] * (int32_t)brow[ki]);
+            c[mi * ldc + ni] = (int32_t)acc;
         }
     }
 }

@@ -37,6 +37,7 @@ void ngo_mat_random_i8(int8_t* out, int64_t rows, int64_t cols, uint64_t seed, i
 /* Config-2 input generator (NOT in the reference; defined and frozen by SURVEY.md 8(d)):
  * Box-Muller over XorShift64Star(seed) 53-bit uniforms, lround(sigma*z), clipped to
  * [-128, 127], row-major fill, one draw pair per element (the cosine branch). */
+void ngo_mat_random_i16(int16_t* out, int64_t rows, int64_t cols, uint64_t seed, int64_t lo, int64_t hi);
 void ngo_mat_normal_i8(int8_t* out, int64_t rows, int64_t cols, uint64_t seed, double sigma);
 
 /* --- GEMM oracles.  A [M x K] u8 row-major (stride lda), B [N x K] i8 row-major (ldb),
@@ -53,6 +54,12 @@ void ngo_gemm_sat_rows(const uint8_t* a, int64_t lda, const int8_t* b, int64_t l
  * (HardwareSaturating), 1 = exact (WideningExact) — the reference SatMode order (lanes.hpp:18). */
 void ngo_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
               int64_t m, int64_t n, int64_t k, int mode, int threads);
+
+/* gemm_ref on i16 x i16 operands (gemm.hpp:36-52 is kind-generic; gemm_sat_oracle defers to
+ * it for i16, gemm.hpp:85): C = sum_k a*b in uint32.  The reference's i16 kernels (pmaddwd
+ * pairs wrap-added, gemm.hpp:161-190) give the same value mod 2^32.  A [M x K], B [N x K]. */
+void ngo_gemm_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                  int64_t m, int64_t n, int64_t k);
 
 /* Pair primitive (lanes.hpp:28-38); mode as above. */
 int32_t ngo_madd_pair(uint8_t a0, uint8_t a1, int8_t b0, int8_t b1, int mode);

@@ -42,7 +42,9 @@ class Oracle:
         L.ngo_mat_random_u8.argtypes = [vp, i64, i64, u64, i64, i64]
         L.ngo_mat_random_i8.argtypes = [vp, i64, i64, u64, i64, i64]
         L.ngo_mat_normal_i8.argtypes = [vp, i64, i64, u64, C.c_double]
+        L.ngo_mat_random_i16.argtypes = [vp, i64, i64, u64, i64, i64]
         L.ngo_gemm.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, C.c_int, C.c_int]
+        L.ngo_gemm_i16.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64]
         L.ngo_madd_pair.argtypes = [C.c_uint8, C.c_uint8, C.c_int8, C.c_int8, C.c_int]
         L.ngo_madd_pair.restype = C.c_int32
         L.ngo_packed_init.argtypes = [C.POINTER(PackedMeta), C.c_int32, C.c_int32, C.c_int32,
@@ -70,6 +72,11 @@ class Oracle:
         self.L.ngo_mat_random_i8(_p(out), rows, cols, seed, lo, hi)
         return out
 
+    def mat_random_i16(self, rows, cols, seed, lo=-32768, hi=32767):
+        out = np.empty((rows, cols), np.int16)
+        self.L.ngo_mat_random_i16(_p(out), rows, cols, seed, lo, hi)
+        return out
+
     def mat_normal_i8(self, rows, cols, seed, sigma=32.0):
         out = np.empty((rows, cols), np.int8)
         self.L.ngo_mat_normal_i8(_p(out), rows, cols, seed, sigma)
@@ -87,6 +94,17 @@ class Oracle:
         if threads is None:
             threads = max(1, min(os.cpu_count() or 1, 64))
         self.L.ngo_gemm(_p(a), k, _p(b), k, _p(c), n, m, n, k, mode, threads)
+        return c
+
+    def gemm_i16(self, a: np.ndarray, b: np.ndarray):
+        """C[m][n] per gemm_ref on i16 x i16 (sum of products mod 2^32)."""
+        a = np.ascontiguousarray(a, np.int16)
+        b = np.ascontiguousarray(b, np.int16)
+        m, k = a.shape
+        n, kb = b.shape
+        assert k == kb
+        c = np.empty((m, n), np.int32)
+        self.L.ngo_gemm_i16(_p(a), k, _p(b), k, _p(c), n, m, n, k)
         return c
 
     def madd_pair(self, a0, a1, b0, b1, mode):
@@ -137,6 +155,7 @@ class Reference:
         L.ref_host_isa_bits.restype = C.c_int
         L.ref_mat_random.argtypes = [C.c_int, i64, i64, C.c_uint64, i64, i64, vp]
         L.ref_gemm.argtypes = [C.c_int, vp, vp, vp, i64, i64, i64, C.c_int, C.c_int, C.c_int]
+        L.ref_gemm_i16.argtypes = [C.c_int, vp, vp, vp, i64, i64, i64]
         L.ref_gemm.restype = C.c_int
         L.ref_pack.argtypes = [vp, i64, i64, C.c_int, C.c_int, C.c_int, i64, i64, i64, C.c_int, vp, i64]
         L.ref_pack.restype = i64
@@ -159,7 +178,7 @@ class Reference:
         return self.L.ref_host_isa_bits()
 
     def mat_random(self, kind: int, rows, cols, seed, lo, hi):
-        out = np.empty((rows, cols), np.uint8 if kind == 0 else np.int8)
+        out = np.empty((rows, cols), {0: np.uint8, 1: np.int8, 2: np.int16, 3: np.int32}[kind])
         self.L.ref_mat_random(kind, rows, cols, seed, lo, hi, _p(out))
         return out
 
@@ -173,6 +192,17 @@ class Reference:
         rc = self.L.ref_gemm(self.VARIANTS[variant], _p(a), _p(b), _p(c), m, n, k, mode, engine, isa_bits)
         if rc != 0:
             raise RuntimeError(f"reference {variant} failed rc={rc}")
+        return c
+
+    def gemm_i16(self, variant: str, a, b):
+        a = np.ascontiguousarray(a, np.int16)
+        b = np.ascontiguousarray(b, np.int16)
+        m, k = a.shape
+        n = b.shape[0]
+        c = np.empty((m, n), np.int32)
+        rc = self.L.ref_gemm_i16({"gemm_ref": 0, "gemm_conventional": 2}[variant], _p(a), _p(b), _p(c), m, n, k)
+        if rc != 0:
+            raise RuntimeError(f"reference i16 {variant} failed rc={rc}")
         return c
 
     def pack(self, a, w, h, v, tm, tn, tk, perm):

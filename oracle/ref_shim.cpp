@@ -102,6 +102,23 @@ int ref_gemm(int variant, const uint8_t* a, const int8_t* b, int32_t* c, int64_t
     }
 }
 
+// i16 x i16 through the unmodified reference: variant 0 = gemm_ref, 2 = gemm_conventional
+// (kernel shape for 16-bit lanes, WideningExact, Engine::Emulated).  Returns 0 on success.
+int ref_gemm_i16(int variant, const int16_t* a, const int16_t* b, int32_t* c, int64_t m, int64_t n, int64_t k) {
+    try {
+        MatrixBuf am(ElemKind::I16, m, k), bm(ElemKind::I16, n, k);
+        std::memcpy(am.bytes(), a, static_cast<size_t>(m * k) * 2);
+        std::memcpy(bm.bytes(), b, static_cast<size_t>(n * k) * 2);
+        MatrixBuf cm = variant == 0 ? gemm_ref(am, bm)
+                                    : gemm_conventional(am, bm, kernel_shape(IsaProfile::v256(), ElemKind::I16),
+                                                        SatMode::WideningExact, Engine::Emulated);
+        std::memcpy(c, cm.bytes(), cm.byte_size());
+        return 0;
+    } catch (const Error&) {
+        return 3;
+    }
+}
+
 // pack_weights with an explicit tile; out has m_pad*k_pad bytes; returns byte size or -1.
 int64_t ref_pack(const uint8_t* a, int64_t m, int64_t k, int w, int h, int v, int64_t tm, int64_t tn,
                  int64_t tk, int perm, uint8_t* out, int64_t out_cap) {

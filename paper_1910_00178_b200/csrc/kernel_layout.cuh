@@ -156,4 +156,36 @@ __global__ void count_mismatch_kernel(const int32_t* __restrict__ x, const int32
     if ((threadIdx.x & 31) == 0 && local) atomicAdd(bad, local);
 }
 
+// i16 operand -> two byte planes for the tensor cores: x = 256 * hi + lo with lo = x & 0xFF
+// (u8) and hi = x >> 8 (s8), so sum_k a*b = 2^16 (ah.bh) + 2^8 (ah.bl + al.bh) + al.bl (mod 2^32)
+// and each term is an int8 tensor-core GEMM.  Planes are K-major with row pitch kp (a multiple
+// of 16, zero-filled past k) — the TMA operand layout.  One thread per 8 elements.
+__global__ void split_i16_kernel(const int16_t* __restrict__ src, int64_t ld, int64_t rows, int64_t k, int64_t kp,
+                                 uint8_t* __restrict__ lo, uint8_t* __restrict__ hi, int vec_ok) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int64_t per_row = kp / 8;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < rows * per_row;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / per_row, c = (i - r * per_row) * 8;
+        const int16_t* p = src + r * ld + c;
+        uint32_t w[4];
+        if (vec_ok && c + 8 <= k) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
+        } else {
+            uint16_t e[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) e[j] = (c + j < k) ? static_cast<uint16_t>(p[j]) : 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j) w[j] = e[2 * j] | (static_cast<uint32_t>(e[2 * j + 1]) << 16);
+        }
+        // little-endian: bytes of w[j] are (lo0, hi0, lo1, hi1)
+        const uint2 l = make_uint2(__byte_perm(w[0], w[1], 0x6420), __byte_perm(w[2], w[3], 0x6420));
+        const uint2 h = make_uint2(__byte_perm(w[0], w[1], 0x7531), __byte_perm(w[2], w[3], 0x7531));
+        *reinterpret_cast<uint2*>(lo + r * kp + c) = l;
+        *reinterpret_cast<uint2*>(hi + r * kp + c) = h;
+    }
+}
+
 }  // namespace ngemm_dev

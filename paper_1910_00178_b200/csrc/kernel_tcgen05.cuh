@@ -68,6 +68,8 @@ struct TileMap {
     int dbg;                       // probes only (NGEMM_TC_DBG): bit 0 skip C stores, bit 1 skip MMAs,
                                    // bit 2 skip operand loads (1-CTA configs)
     int trace_id;                  // trace build: launch index for the phase stamps (-1 otherwise)
+    int a_signed, b_signed;        // operand formats (u8 x s8 for the NGEMM path; any mix for i16 planes)
+    int shift;                     // epilogue: C (+)= acc << shift  (i16 byte-plane decomposition)
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -231,7 +233,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (single thread of the leader CTA)
-            constexpr uint32_t idesc = idesc_i8(UMMA_M, BN, /*a_signed=*/false, /*b_signed=*/true);
+            const uint32_t idesc = idesc_i8(UMMA_M, BN, map.a_signed != 0, map.b_signed != 0);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
@@ -290,6 +292,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 tmem_ld_32x32b_x32(taddr + c, v);
                 tmem_wait_ld();
                 if (!has_k || row0 >= M) continue;
+                if (map.shift) {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) v[j] <<= map.shift;  // mod 2^32, like the accumulator
+                }
                 const int col0 = tn * BN + c;
                 if (c_mode != 2) {
                     uint8_t* buf = stage_c + cbuf * S::STAGE_C_BYTES;

@@ -698,10 +698,18 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
     return best;
 }
 
+// Operand formats and epilogue of one tcgen05 launch: the NGEMM path is u8 x s8 into C; the
+// i16 path issues four launches over byte planes with mixed formats, shifting and adding into C.
+struct TcOps {
+    int a_signed = 0, b_signed = 1;
+    int shift = 0;       // C (+)= acc << shift
+    int accumulate = 0;  // 1: TMA reduce-add into C (C holds the previous planes' sum)
+};
+
 template <int BN, int STAGES, int CG, int MC = 1>
 ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcmap, int32_t* c,
                          int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int c_mode, const DevInfo& di,
-                         cudaStream_t st, const int32_t* guard) {
+                         cudaStream_t st, const int32_t* guard, const TcOps& ops) {
     using S = tc::Smem<BN, STAGES, CG>;
     auto kern = tc_gemm_kernel<BN, STAGES, CG, MC>;
     static std::once_flag once[64];
@@ -727,12 +735,17 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.prefetch = l2_prefetch_enabled() ? 1 : 0;
     map.dbg = 0;
     map.trace_id = -1;
+    map.a_signed = ops.a_signed;
+    map.b_signed = ops.b_signed;
+    map.shift = ops.shift;
 #ifdef NGEMM_TRACE
     if (const char* e = std::getenv("NGEMM_TC_DBG")) map.dbg = std::atoi(e);  // trace build only
     map.trace_id = g_trace_next++;
 #endif
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
-    if (map.splits > 1) {
+    if (ops.accumulate) {
+        c_mode = 1;  // C already holds a partial sum: every split reduce-adds into it
+    } else if (map.splits > 1) {
         c_mode = 1;
         ngemm_status zs = zero_c(c, ldc, m, n, guard, 1, di, st);
         if (zs != NGEMM_OK) return zs;
@@ -745,7 +758,7 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 
 ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                             int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
-                            const int32_t* guard = nullptr) {
+                            const int32_t* guard = nullptr, const TcOps& ops = TcOps()) {
     // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3): stage ragged
     // operands through a zero-padded scratch copy (padding K at the end is neutral).
     const uint8_t* a_use = a;
@@ -778,15 +791,16 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
     if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, ci.bn / ci.cg);
     if (s == NGEMM_OK && c_tma) s = make_tmap_c(&tcm, c, m, n, ldc);
     const int c_mode = c_tma ? 0 : 2;
+    if (ops.accumulate && !c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "tcgen05: accumulating epilogue needs a TMA-describable C");
     if (s == NGEMM_OK) {
         switch (plan.cfg) {
-        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
-        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
-        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
-        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
-        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
-        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
-        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard); break;
+        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
         }
     }
     if (scratch) cudaFreeAsync(scratch, st);
@@ -1018,6 +1032,51 @@ struct ngemm_packed_dev {
 
 namespace {
 
+// i16 x i16 on the tensor cores: split both operands into byte planes (split_i16_kernel), then
+// four int8 tcgen05 GEMMs with per-launch operand formats —
+//   C  = lo(A).lo(B)                 u8 x u8
+//   C += (lo(A).hi(B)) << 8          u8 x s8   (TMA reduce-add epilogue)
+//   C += (hi(A).lo(B)) << 8          s8 x u8
+//   C += (hi(A).hi(B)) << 16         s8 x s8
+// exact mod 2^32 like the reference's wrapping pair accumulation (gemm.hpp:161-190).
+ngemm_status launch_i16_tc(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+                           int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
+    const int64_t kp = round_up(k, 16);
+    uint8_t* planes = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&planes), static_cast<size_t>(2 * (m + n) * kp), st));
+    uint8_t* al = planes;
+    uint8_t* ah = al + m * kp;
+    uint8_t* bl = ah + m * kp;
+    uint8_t* bh = bl + n * kp;
+    ngemm_status s = NGEMM_OK;
+    auto split = [&](const int16_t* x, int64_t ld, int64_t rows, uint8_t* lo, uint8_t* hi) {
+        if (s != NGEMM_OK) return;
+        const int vec = reinterpret_cast<uintptr_t>(x) % 16 == 0 && ld % 8 == 0;
+        const int64_t work = rows * (kp / 8);
+        const int blocks = static_cast<int>(std::min<int64_t>((work + 255) / 256, 8LL * di.sms));
+        cudaError_t e = launch_k(split_i16_kernel, dim3(blocks), dim3(256), 0, st, 1, 1, x, ld, rows, k, kp, lo, hi, vec);
+        if (e != cudaSuccess) s = fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+        else g_launches.fetch_add(1, std::memory_order_relaxed);
+    };
+    split(a, lda, m, al, ah);
+    split(b, ldb, n, bl, bh);
+    struct Term {
+        const uint8_t* x;
+        const uint8_t* y;
+        TcOps ops;
+    };
+    const Term terms[4] = {{al, bl, {0, 0, 0, 0}}, {al, bh, {0, 1, 8, 1}}, {ah, bl, {1, 0, 8, 1}}, {ah, bh, {1, 1, 16, 1}}};
+    for (const Term& t : terms) {
+        if (s != NGEMM_OK) break;
+        s = launch_tcgen05(t.x, kp, reinterpret_cast<const int8_t*>(t.y), kp, c, ldc, m, n, kp, di, st, nullptr, t.ops);
+    }
+    cudaFreeAsync(planes, st);
+    return s;
+}
+
+// i16 GEMMs with at least this many MACs (and M > 16, TMA-describable C) use the tensor cores.
+constexpr double kI16TensorMinWork = 1 << 22;
+
 ngemm_status run_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ldb, int32_t* c, int64_t ldc, int64_t m,
                      int64_t n, int64_t k, cudaStream_t st) {
     ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, NGEMM_SAT_EXACT);
@@ -1026,6 +1085,11 @@ ngemm_status run_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ld
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
+    const bool c_tma = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (ldc % 4 == 0);
+    bool tensor = c_tma && m > kSkinnyMaxM && static_cast<double>(m) * n * k >= kI16TensorMinWork &&
+                  m <= INT32_MAX / 2 && k <= INT32_MAX / 4;
+    if (const char* e = std::getenv("NGEMM_I16_PATH")) tensor = c_tma && std::strcmp(e, "tcgen05") == 0;  // tests
+    if (tensor) return launch_i16_tc(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     return launch_simt_i16(a, lda, b, ldb, c, ldc, m, n, k, st);
 }
 

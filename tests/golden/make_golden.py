@@ -129,6 +129,20 @@ def main():
                 c4.append({"size": s, "a": pa, "b": pb, "exact": int(ce[0, 0]), "sat": int(cs[0, 0])})
     g["config4"] = c4
 
+    # --- i16 x i16 (gemm_ref and the emulated 16-bit gemm_conventional, gemm.hpp:161-190):
+    # inputs from the reference's own mat_random(I16); the extreme case wraps mod 2^32
+    i16 = []
+    for (m, n, k, seed, lo, hi) in [(1, 1, 1, 3, -32768, 32767), (7, 5, 3, 4, -32768, 32767),
+                                    (33, 17, 129, 5, -32768, 32767), (64, 48, 96, 6, -300, 300),
+                                    (5, 9, 4096, 7, -32768, -32768), (40, 24, 1000, 8, -32768, 32767)]:
+        a16 = ref.mat_random(2, m, k, seed, lo, hi)
+        b16 = ref.mat_random(2, n, k, seed + 100, lo, hi)
+        c_ref = ref.gemm_i16("gemm_ref", a16, b16)
+        assert (ref.gemm_i16("gemm_conventional", a16, b16) == c_ref).all()
+        i16.append({"m": m, "n": n, "k": k, "seed": seed, "lo": lo, "hi": hi, "a_fnv": fnv(a16),
+                    "c_fnv": fnv(c_ref), "c_sum": int(c_ref.astype(np.int64).sum())})
+    g["i16"] = i16
+
     # --- config 1 (1024^3, A seed 0 / B seed 1), both modes through the reference oracles
     t0 = time.time()
     A = ref.mat_random(U8, 1024, 1024, 0, 0, 255)

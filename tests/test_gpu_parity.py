@@ -441,3 +441,36 @@ def test_batched_broadcast_and_api(cuda, oracle):
     with pytest.raises(api.ShapeError):
         api.gemm_device_batched(torch.zeros((2, 4, 8), dtype=torch.uint8, device="cuda"),
                                 torch.zeros((3, 4, 8), dtype=torch.int8, device="cuda"))
+
+
+def _dev_gemm_i16(a, b):
+    import torch
+    m, k = a.shape
+    n = b.shape[0]
+    da, db = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    frame = torch.full((m + 16, n), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+    L = _lib.load()
+    _lib.check(L.ngemm_cuda_gemm_i16(da.data_ptr(), k, db.data_ptr(), k, frame[8:8 + m].data_ptr(), n, m, n, k,
+                                     torch.cuda.current_stream().cuda_stream))
+    torch.cuda.synchronize()
+    full = frame.cpu().numpy()
+    assert (full[:8] == 0x5A5A5A5A).all() and (full[8 + m:] == 0x5A5A5A5A).all(), "i16 kernel wrote outside C"
+    return full[8:8 + m]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("path", ["simt", "tcgen05"])
+def test_i16_paths_vs_reference_golden(cuda, oracle, golden, path, monkeypatch):
+    """i16 x i16 (gemm.hpp:161-190): the CUDA-core kernel and the tensor-core byte-plane
+    decomposition (4 int8 tcgen05 GEMMs, shifted and reduce-added) against the reference."""
+    monkeypatch.setenv("NGEMM_I16_PATH", path)
+    for c in golden["i16"]:
+        a = oracle.mat_random_i16(c["m"], c["k"], c["seed"], c["lo"], c["hi"])
+        b = oracle.mat_random_i16(c["n"], c["k"], c["seed"] + 100, c["lo"], c["hi"])
+        out = _dev_gemm_i16(a, b)
+        assert oracle.fnv1a(out) == c["c_fnv"], (path, c)
+    rng = np.random.default_rng(11)
+    for (m, n, k) in [(300, 129, 777), (17, 64, 16), (256, 512, 4096), (1000, 1000, 1000)]:
+        a = rng.integers(-32768, 32768, size=(m, k), dtype=np.int16)
+        b = rng.integers(-32768, 32768, size=(n, k), dtype=np.int16)
+        assert (_dev_gemm_i16(a, b) == oracle.gemm_i16(a, b)).all(), (path, m, n, k)

@@ -193,3 +193,14 @@ def test_oracle_matches_reference_directly(oracle):
         assert (oracle.gemm(a, b, EXACT) == ref.gemm("gemm_ref", a, b)).all()
         assert (oracle.gemm(a, b, SAT) == ref.gemm("gemm_sat_oracle", a, b)).all()
         assert (oracle.gemm(a, b, SAT) == ref.gemm("gemm_conventional", a, b, SAT, engine=0)).all()
+
+
+def test_i16_oracle_vs_reference_golden(oracle, golden):
+    # inputs: the reference's mat_random(I16) restated; outputs: gemm_ref on i16 (gemm.hpp:36-52),
+    # which the reference's emulated 16-bit gemm_conventional matched when the fixture was made
+    for c in golden["i16"]:
+        a = oracle.mat_random_i16(c["m"], c["k"], c["seed"], c["lo"], c["hi"])
+        b = oracle.mat_random_i16(c["n"], c["k"], c["seed"] + 100, c["lo"], c["hi"])
+        assert oracle.fnv1a(a) == c["a_fnv"]
+        out = oracle.gemm_i16(a, b)
+        assert oracle.fnv1a(out) == c["c_fnv"] and int(out.astype(np.int64).sum()) == c["c_sum"]
