@@ -641,11 +641,10 @@ constexpr TcCfgInfo kTcCfg[TC_NUM_CFG] = {
     {1, 128, 1, 450.0, 1},  // 128x128, 2 stages: latency-limited stream, but co-resident
     {1, 64, 1, 330.0, 1},   // 128x64, 3 stages
 };
-// A launch whose CTAs cannot share an SM with the previous grid's pays the full CTA launch +
-// barrier/TMEM setup after that grid drains (~1.5 us more per launch than a lean
-// configuration, profiles/tc_trace_r1.log); lean CTAs become resident early under PDL and do
-// their setup and L2 prefetch while the previous grid still runs.
-constexpr double kNotLeanCycles = 2800.0;
+// Lean configurations fit two CTAs per SM, so under PDL the next grid's CTAs finish their setup
+// while the previous grid runs — but their 2-3 stage pipelines lose more in the K loop than the
+// overlap saves (profiles/tc_trace_r1.log, sweep_tc_cfg_r1.log): the planner skips them; the
+// autotuner still tries them.
 
 struct TcPlan {
     int cfg, splits;
@@ -670,6 +669,7 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
         const TcCfgInfo& ci = kTcCfg[cfg];
         const int64_t tiles_n = (n + ci.bn - 1) / ci.bn;
         if (ci.mc > 1 && (tiles_n % ci.mc != 0 || quad_disabled())) continue;
+        if (ci.lean) continue;
         const int64_t tiles = ((m + 128 * ci.cg - 1) / (128 * ci.cg)) * tiles_n / ci.mc;
         const int64_t units = sms / (ci.cg * ci.mc);
         for (int splits = 1; splits <= 16; splits *= 2) {
@@ -678,7 +678,6 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
             const int64_t waves = (work + units - 1) / units;
             const double kb = static_cast<double>((num_kb + splits - 1) / splits);
             double t = static_cast<double>(waves) * kb * ci.cycles_per_kb + 600.0 + ci.bn * 8.0;
-            if (!ci.lean) t += kNotLeanCycles;
             if (splits > 1) t += 1500.0;                 // zeroing C + reduce-add traffic
             if (ci.cg == 2) t *= 0.97;                    // less L2->SM traffic per MAC
             if (ci.mc == 2) t *= 0.98;                    // A multicast: a further 25% less
