@@ -1101,20 +1101,27 @@ bool is_pinned(const void* p) {
     return attr.type == cudaMemoryTypeHost;
 }
 
-// Large GEMM on PINNED host buffers: A is streamed in row chunks on a copy-in stream, each
-// chunk's GEMM runs on a compute stream as soon as its rows (and B) have landed, and its C
-// rows go back on a copy-out stream — H2D, tensor-core compute and D2H overlap across chunks
-// (PCIe is full duplex), instead of copy-all / compute / copy-all.
+// Large GEMM on PINNED host buffers, pipelined over a ti x tj grid of C tiles (column passes):
+// A's row blocks and B's row blocks (= C's column blocks) stream in on a copy-in stream in
+// first-use order,
+// each tile's GEMM runs on a compute stream as soon as its A and B blocks have landed, and its C
+// tile goes back on a copy-out stream (a pitched D2H into the row-major host C).  H2D, tensor-
+// core compute and D2H overlap (PCIe is full duplex); tiling B as well as A lets the first C
+// bytes leave after 1/ti + 1/tj of the operands have arrived instead of after all of B, so the
+// end-to-end time approaches the D2H of C alone.
 ngemm_status host_gemm_pipelined(const uint8_t* a, const int8_t* b, int32_t* c, int64_t m, int64_t n, int64_t k,
                                  int sat_mode, int kernel) {
     const int64_t kp = round_up(k, 16);
-    const int64_t chunk = round_up((m + 7) / 8, 256);
-    const int nchunks = static_cast<int>((m + chunk - 1) / chunk);
+    const int ti_want = 8, tj_want = n >= 4096 ? 4 : 1;
+    const int64_t rchunk = round_up((m + ti_want - 1) / ti_want, 256);
+    const int64_t cchunk = round_up((n + tj_want - 1) / tj_want, 256);
+    const int ti = static_cast<int>((m + rchunk - 1) / rchunk), tj = static_cast<int>((n + cchunk - 1) / cchunk);
     const size_t a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
     const size_t c_bytes = static_cast<size_t>(m * n) * 4;
     const size_t b_off = round_up(static_cast<int64_t>(a_bytes), 256), c_off = b_off + round_up(b_bytes, 256);
     cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
-    std::vector<cudaEvent_t> ev(static_cast<size_t>(2 * nchunks + 2), nullptr);
+    // events: A blocks [0, ti), B blocks [ti, ti + tj), C tiles after, one "done"
+    std::vector<cudaEvent_t> ev(static_cast<size_t>(ti + tj + ti * tj + 1), nullptr);
     ngemm_status s = NGEMM_OK;
     auto ck = [&](cudaError_t e, const char* what) {
         if (e != cudaSuccess && s == NGEMM_OK) s = fail(NGEMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -1126,24 +1133,43 @@ ngemm_status host_gemm_pipelined(const uint8_t* a, const int8_t* b, int32_t* c, 
     for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     uint8_t* buf = nullptr;
     if (s == NGEMM_OK && ck(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, sin), "malloc")) {
-        cudaEvent_t ev_b = ev[0], ev_done = ev[1];
-        ck(copy_rows_h2d(buf + b_off, kp, b, k, n, sin), "H2D B");
-        ck(cudaEventRecord(ev_b, sin), "record");
-        ck(cudaStreamWaitEvent(scomp, ev_b, 0), "wait");
-        for (int i = 0; i < nchunks && s == NGEMM_OK; ++i) {
-            const int64_t r0 = i * chunk, rows = std::min(chunk, m - r0);
-            cudaEvent_t ev_a = ev[2 + 2 * i], ev_c = ev[3 + 2 * i];
-            ck(copy_rows_h2d(buf + r0 * kp, kp, a + r0 * k, k, rows, sin), "H2D A");
-            ck(cudaEventRecord(ev_a, sin), "record");
-            ck(cudaStreamWaitEvent(scomp, ev_a, 0), "wait");
-            if (s == NGEMM_OK)
-                s = run_gemm(buf + r0 * kp, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp,
-                             reinterpret_cast<int32_t*>(buf + c_off) + r0 * n, n, rows, n, k, sat_mode, kernel, scomp);
-            ck(cudaEventRecord(ev_c, scomp), "record");
-            ck(cudaStreamWaitEvent(sout, ev_c, 0), "wait");
-            ck(cudaMemcpyAsync(c + r0 * n, buf + c_off + static_cast<size_t>(r0 * n) * 4,
-                               static_cast<size_t>(rows * n) * 4, cudaMemcpyDeviceToHost, sout), "D2H C");
+        int32_t* dc = reinterpret_cast<int32_t*>(buf + c_off);
+        // column pass j over all row blocks i: the first pass streams A block by block behind
+        // B block 0, so the first C tile leaves after A_0 + B_0 (1/8 + 1/4 of the operands)
+        // and the copy-in keeps pace with the copy-out; later passes only add one B block.
+        for (int j = 0; j < tj && s == NGEMM_OK; ++j) {
+            const int64_t c0 = j * cchunk, cols = std::min(cchunk, n - c0);
+            for (int i = 0; i < ti && s == NGEMM_OK; ++i) {
+                const int64_t r0 = i * rchunk, rows = std::min(rchunk, m - r0);
+                if (j == 0) {
+                    if (i == 0) {
+                        ck(copy_rows_h2d(buf + b_off, kp, b, k, cols, sin), "H2D B");
+                        ck(cudaEventRecord(ev[ti], sin), "record");
+                    }
+                    ck(copy_rows_h2d(buf + r0 * kp, kp, a + r0 * k, k, rows, sin), "H2D A");
+                    ck(cudaEventRecord(ev[i], sin), "record");
+                } else if (i == 0) {
+                    ck(copy_rows_h2d(buf + b_off + c0 * kp, kp, b + c0 * k, k, cols, sin), "H2D B");
+                    ck(cudaEventRecord(ev[ti + j], sin), "record");
+                }
+                ck(cudaStreamWaitEvent(scomp, ev[i], 0), "wait");
+                ck(cudaStreamWaitEvent(scomp, ev[ti + j], 0), "wait");
+                if (s == NGEMM_OK)
+                    s = run_gemm(buf + r0 * kp, kp, reinterpret_cast<const int8_t*>(buf + b_off + c0 * kp), kp,
+                                 dc + r0 * n + c0, n, rows, cols, k, sat_mode, kernel, scomp);
+                cudaEvent_t ev_c = ev[ti + tj + i * tj + j];
+                ck(cudaEventRecord(ev_c, scomp), "record");
+                ck(cudaStreamWaitEvent(sout, ev_c, 0), "wait");
+                if (tj == 1)
+                    ck(cudaMemcpyAsync(c + r0 * n, dc + r0 * n, static_cast<size_t>(rows * n) * 4,
+                                       cudaMemcpyDeviceToHost, sout), "D2H C");
+                else
+                    ck(cudaMemcpy2DAsync(c + r0 * n + c0, static_cast<size_t>(n) * 4, dc + r0 * n + c0,
+                                         static_cast<size_t>(n) * 4, static_cast<size_t>(cols) * 4,
+                                         static_cast<size_t>(rows), cudaMemcpyDeviceToHost, sout), "D2H C");
+            }
         }
+        cudaEvent_t ev_done = ev.back();
         ck(cudaEventRecord(ev_done, sout), "record");
         cudaStreamWaitEvent(sin, ev_done, 0);
         cudaFreeAsync(buf, sin);

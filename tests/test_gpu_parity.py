@@ -362,17 +362,18 @@ def test_host_entry_pipelined_pinned(cuda, oracle):
     """ngemm_cuda_gemm_u8i8_host on PINNED host buffers takes the chunked H2D/compute/D2H
     pipeline (C >= 64 MiB); result must equal the oracle in both modes."""
     import torch
-    m, n, k = 4096, 4096, 640
-    a = oracle.mat_random_u8(m, k, 11)
-    b = oracle.mat_random_i8(n, k, 12)
-    ta = torch.from_numpy(a).pin_memory()
-    tb = torch.from_numpy(b).pin_memory()
-    tc = torch.empty((m, n), dtype=torch.int32).pin_memory()
     L = _lib.load()
-    for mode in (EXACT, SAT):
-        tc.fill_(-1)
-        _lib.check(L.ngemm_cuda_gemm_u8i8_host(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), m, n, k, mode, 0))
-        assert (tc.numpy() == oracle.gemm(a, b, mode)).all(), mode
+    # 4096^2 splits into 8 x 4 C tiles; 4000 x 4500 x 333 gives ragged row/column tiles and padded K
+    for (m, n, k) in [(4096, 4096, 640), (4000, 4500, 333)]:
+        a = oracle.mat_random_u8(m, k, 11)
+        b = oracle.mat_random_i8(n, k, 12)
+        ta = torch.from_numpy(a).pin_memory()
+        tb = torch.from_numpy(b).pin_memory()
+        tc = torch.empty((m, n), dtype=torch.int32).pin_memory()
+        for mode in (EXACT, SAT):
+            tc.fill_(-1)
+            _lib.check(L.ngemm_cuda_gemm_u8i8_host(ta.data_ptr(), tb.data_ptr(), tc.data_ptr(), m, n, k, mode, 0))
+            assert (tc.numpy() == oracle.gemm(a, b, mode)).all(), (m, n, k, mode)
 
 
 def test_autotuner_picks_verified_config_and_dispatch_stays_exact(cuda, oracle, tmp_path):
