@@ -64,7 +64,6 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
 
     const int tid = threadIdx.x;
     const int tx = tid & 15, ty = tid >> 4;
-    const int32_t one = (k_split > 0) ? 1 : 0;  // a runtime 1 the compiler cannot fold
     const int64_t m0 = static_cast<int64_t>(blockIdx.y) * TILE;
     const int64_t n0 = static_cast<int64_t>(blockIdx.x) * TILE;
     const int64_t kb = static_cast<int64_t>(blockIdx.z) * k_split;
@@ -146,13 +145,7 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
                 for (int i = 0; i < TT; ++i) {
                     const uint32_t alo = a[i] & 0x0000FFFFu, ahi = a[i] & 0xFFFF0000u;
 #pragma unroll
-                    for (int j = 0; j < TT; ++j) {
-                        const int32_t p0 = clamp_i16(dp4a_us(alo, b[j], 0));
-                        const int32_t p1 = clamp_i16(dp4a_us(ahi, b[j], 0));
-                        // the two clamps already occupy the ALU pipe (VIMNMX); accumulate on the
-                        // FMA pipe (IMAD with a runtime 1) to balance the two pipes
-                        acc[i][j] = imad_u32(p0, one, imad_u32(p1, one, acc[i][j]));
-                    }
+                    for (int j = 0; j < TT; ++j) acc[i][j] = sat_word_add(alo, ahi, b[j], acc[i][j]);
                 }
             }
         }

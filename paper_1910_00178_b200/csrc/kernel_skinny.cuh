@@ -122,12 +122,8 @@ __global__ void __launch_bounds__(skinny::THREADS)
                         for (int q = 0; q < 4; ++q) s = dp4a_us(aw[q], bw[q], s);
                     } else {
 #pragma unroll
-                        for (int q = 0; q < 4; ++q) {
-                            const int32_t p0 = clamp_i16(dp4a_us(aw[q] & 0x0000FFFFu, bw[q], 0));
-                            const int32_t p1 = clamp_i16(dp4a_us(aw[q] & 0xFFFF0000u, bw[q], 0));
-                            s = static_cast<int32_t>(static_cast<uint32_t>(s) + static_cast<uint32_t>(p0) +
-                                                     static_cast<uint32_t>(p1));
-                        }
+                        for (int q = 0; q < 4; ++q)
+                            s = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], s);
                     }
                     acc[m * NR + r] = s;
                 }
@@ -233,12 +229,8 @@ __global__ void __launch_bounds__(skinny_rows::THREADS)
                 for (int q = 0; q < 8; ++q) sacc = dp4a_us(aw[q], bw[q], sacc);
             } else {
 #pragma unroll
-                for (int q = 0; q < 8; ++q) {
-                    const int32_t p0 = clamp_i16(dp4a_us(aw[q] & 0x0000FFFFu, bw[q], 0));
-                    const int32_t p1 = clamp_i16(dp4a_us(aw[q] & 0xFFFF0000u, bw[q], 0));
-                    sacc = static_cast<int32_t>(static_cast<uint32_t>(sacc) + static_cast<uint32_t>(p0) +
-                                                static_cast<uint32_t>(p1));
-                }
+                for (int q = 0; q < 8; ++q)
+                    sacc = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], sacc);
             }
             acc[m] = sacc;
         }
@@ -482,7 +474,6 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
     pdl_wait();
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
-    const int32_t one = (K > 0) ? 1 : 0;  // runtime 1 (keeps the adds on the FMA pipe)
 
     auto load16 = [&](const uint8_t* X, int64_t ld, int64_t rows, int64_t row, int64_t k, bool stream) -> uint4 {
         uint4 v = make_uint4(0, 0, 0, 0);
@@ -529,11 +520,7 @@ __global__ void __launch_bounds__(WARPS * 32)
                     const uint32_t bw[4] = {bv[r][c].x, bv[r][c].y, bv[r][c].z, bv[r][c].w};
                     int32_t s = acc[r * MT + m];
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        const int32_t p0 = clamp_i16(dp4a_us(aw[q] & 0x0000FFFFu, bw[q], 0));
-                        const int32_t p1 = clamp_i16(dp4a_us(aw[q] & 0xFFFF0000u, bw[q], 0));
-                        s = imad_u32(p0, one, imad_u32(p1, one, s));
-                    }
+                    for (int q = 0; q < 4; ++q) s = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], s);
                     acc[r * MT + m] = s;
                 }
             }

@@ -22,6 +22,22 @@ __device__ __forceinline__ int32_t dp4a_us(uint32_t a, uint32_t b, int32_t c) {
 
 __device__ __forceinline__ int32_t clamp_i16(int32_t x) { return max(-32768, min(32767, x)); }
 
+// HardwareSaturating step for one 4-byte K word (the VPMADDUBSW + VPMADDWD pair, lanes.hpp:28-33,
+// simd_native.hpp:144-178): the two even-aligned pair sums p0 = a0 b0 + a1 b1 and
+// p1 = a2 b2 + a3 b3 come from IDP.4A on the masked halves of a (alo = a & 0xFFFF,
+// ahi = a & 0xFFFF0000), one I2IP.S16.S32.SAT packs both with int16 saturation, and one
+// IDP.2A (dot with the bytes {1, 1}) wrap-adds both halves into acc: 4 instructions per word
+// instead of 2 IDP + 4 VIMNMX clamps + 2 adds.
+__device__ __forceinline__ int32_t sat_word_add(uint32_t alo, uint32_t ahi, uint32_t b, int32_t acc) {
+    const int32_t p0 = dp4a_us(alo, b, 0);
+    const int32_t p1 = dp4a_us(ahi, b, 0);
+    uint32_t packed;
+    asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(packed) : "r"(p1), "r"(p0));
+    int32_t r;
+    asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(packed), "r"(0x0101), "r"(acc));
+    return r;
+}
+
 // a * b + c on the FMA pipe (IMAD), wrapping mod 2^32.
 __device__ __forceinline__ int32_t imad_u32(int32_t a, int32_t b, int32_t c) {
     int32_t d;
