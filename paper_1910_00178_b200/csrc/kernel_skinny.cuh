@@ -475,54 +475,60 @@ __global__ void __launch_bounds__(WARPS * 32)
     pdl_wait();
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
 
-    auto load16 = [&](const uint8_t* X, int64_t ld, int64_t rows, int64_t row, int64_t k, bool stream) -> uint4 {
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (row >= rows || k >= K) return v;
-        const uint8_t* p = X + row * ld + k;
-        if (vec_ok && k + 16 <= K) {
-            if (stream)
-                asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0,%1,%2,%3}, [%4];"
-                             : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-            else
-                v = __ldg(reinterpret_cast<const uint4*>(p));
-            return v;
-        }
-        uint32_t w[4] = {0, 0, 0, 0};
-#pragma unroll
-        for (int i = 0; i < 16; ++i)
-            if (k + i < K) w[i >> 2] |= static_cast<uint32_t>(__ldg(p + i)) << (8 * (i & 3));
-        return make_uint4(w[0], w[1], w[2], w[3]);
-    };
-
     int32_t acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0;
+    // A row m, half c of the current chunk (aw) against both B rows (bv): 4 K words each
+    auto consume = [&](const uint4 (&bv)[2][2], int m, int c, const uint4& av) {
+        const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+        for (int r = 0; r < 2; ++r) {
+            const uint32_t bw[4] = {bv[r][c].x, bv[r][c].y, bv[r][c].z, bv[r][c].w};
+            int32_t s = acc[r * MT + m];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) s = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], s);
+            acc[r * MT + m] = s;
+        }
+    };
 
     const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
-    const int64_t chunks = (min(K, kbeg + k_range) - kbeg + 127) / 128;
-#pragma unroll 2
+    const int64_t kend = min(K, kbeg + k_range);
+    const int64_t chunks = (kend - kbeg + 127) / 128;
+    const bool vec = vec_ok != 0, rows_full = n0 + 16 <= N;
+    const uint8_t* pb = Bu + (n0 + g) * ldb + t * 16;  // thread t reads bytes [c*64 + t*16, +16) of a chunk
+    const uint8_t* pa = A + t * 16;
+#pragma unroll 1
     for (int64_t ch = warp; ch < chunks; ch += WARPS) {
         const int64_t k0 = kbeg + ch * 128;  // k_range is a multiple of 128: pairs stay even-aligned
         uint4 bv[2][2];
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            bv[0][c] = load16(Bu, ldb, N, n0 + g, k0 + c * 64 + t * 16, true);
-            bv[1][c] = load16(Bu, ldb, N, n0 + g + 8, k0 + c * 64 + t * 16, true);
-        }
-#pragma unroll
-        for (int m = 0; m < MT; ++m) {
+        if (vec && rows_full && k0 + 128 <= kend) {
+            // whole chunk in range (warp-uniform): unconditional 16-byte loads
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const uint4 av = load16(A, lda, M, m, k0 + c * 64 + t * 16, false);
-                const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+                bv[0][c] = load16_row<true>(pb + k0 + c * 64, 16, true);
+                bv[1][c] = load16_row<true>(pb + 8 * ldb + k0 + c * 64, 16, true);
+            }
 #pragma unroll
-                for (int r = 0; r < 2; ++r) {
-                    const uint32_t bw[4] = {bv[r][c].x, bv[r][c].y, bv[r][c].z, bv[r][c].w};
-                    int32_t s = acc[r * MT + m];
+            for (int m = 0; m < MT; ++m) {
+                if (m >= M) break;  // uniform
 #pragma unroll
-                    for (int q = 0; q < 4; ++q) s = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], s);
-                    acc[r * MT + m] = s;
-                }
+                for (int c = 0; c < 2; ++c)
+                    consume(bv, m, c, __ldg(reinterpret_cast<const uint4*>(pa + m * lda + k0 + c * 64)));
+            }
+        } else {
+            // ragged chunk (K tail, last row group, unaligned operands): bounded loads, zero fill
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int64_t rem = kend - (k0 + c * 64 + t * 16);
+                bv[0][c] = load16_row<true>(pb + k0 + c * 64, (n0 + g < N) ? rem : 0, vec);
+                bv[1][c] = load16_row<true>(pb + 8 * ldb + k0 + c * 64, (n0 + g + 8 < N) ? rem : 0, vec);
+            }
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                if (m >= M) break;
+#pragma unroll
+                for (int c = 0; c < 2; ++c)
+                    consume(bv, m, c, load16_row<false>(pa + m * lda + k0 + c * 64, kend - (k0 + c * 64 + t * 16), vec));
             }
         }
     }

@@ -583,8 +583,9 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
     // Measured on B200 (profiles/sweep_r1_skinny*.log): exact -> the warp-MMA load stream (3),
     // fastest on 11 of the 12 c2 shapes (1.9-4.5 us; the tcgen05 swap-AB kernel (2) pays
     // ~1 us more for TMEM/mbarrier/cluster setup); saturating -> the dp4a load stream (4),
-    // except M > 4 with few B rows where the lanes-own-rows broadcast kernel (1) wins.
-    int variant = mode == NGEMM_SAT_EXACT ? 3 : ((m > 4 && n < 2048) ? 1 : 4);
+    // which since the pack-saturate step also beats the broadcast kernel (1) on every
+    // M > 4, N < 2048 shape (profiles/sweep_r1_skinny_sat_variants.log).
+    int variant = mode == NGEMM_SAT_EXACT ? 3 : 4;
     if (const char* v = std::getenv("NGEMM_SKINNY_VARIANT")) variant = std::atoi(v);  // experiments
     if (t_force.skinny_variant >= 0) variant = t_force.skinny_variant;
     if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
