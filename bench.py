@@ -380,7 +380,7 @@ def run_ours(args):
         line = {
             "metric": "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T",
             "value": round(value, 2), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": round(ms_step, 4), "higher_is_better": True,
+            "warmup": args.warmup, "ms_per_step": round(ms_step, 6), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8*s8->s32",
             "data": "synthetic: A uniform u8 [0,255], B uniform i8 [-128,127] (torch generators seed 0/1, on device)",
             "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode,

@@ -394,11 +394,30 @@ __global__ void __launch_bounds__(WARPS * 32)
         }
     };
 
+    // whole chunks with both B rows in range (warp-uniform): unconditional 16-byte loads; A rows
+    // past M read row 0 and are zeroed by a select (no branch)
+    auto load_chunk_fast = [&](int64_t ch, uint4 (&bv)[2][2], uint4 (&av)[NB][2]) {
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int64_t o = ch * skinny_mma::CHUNK + c * 64;
+            bv[0][c] = load16_row<true>(pb + o, 16, true);
+            bv[1][c] = load16_row<true>(pb + 8 * ldb + o, 16, true);
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+                const bool ok = nb * 8 + g < M;
+                const uint4 v = __ldg(reinterpret_cast<const uint4*>((ok ? pa + nb * 8 * lda : A + kt) + o));
+                av[nb][c] = ok ? v : make_uint4(0, 0, 0, 0);
+            }
+        }
+    };
+
     const int64_t chunks = (kend - kbeg + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
+    const int64_t fast_chunks = ((vec_ok & 4) && n0 + 16 <= N) ? (kend - kbeg) / skinny_mma::CHUNK : 0;
 #pragma unroll 4
     for (int64_t ch = ks; ch < chunks; ch += KS) {
         uint4 bv[2][2], av[NB][2];
-        load_chunk(ch, bv, av);
+        if (ch < fast_chunks) load_chunk_fast(ch, bv, av);
+        else load_chunk(ch, bv, av);
         compute(bv, av);
     }
 
@@ -501,7 +520,7 @@ __global__ void __launch_bounds__(WARPS * 32)
     for (int64_t ch = warp; ch < chunks; ch += WARPS) {
         const int64_t k0 = kbeg + ch * 128;  // k_range is a multiple of 128: pairs stay even-aligned
         uint4 bv[2][2];
-        if (vec && rows_full && k0 + 128 <= kend) {
+        if ((vec_ok & 4) && rows_full && k0 + 128 <= kend) {
             // whole chunk in range (warp-uniform): unconditional 16-byte loads
 #pragma unroll
             for (int c = 0; c < 2; ++c) {

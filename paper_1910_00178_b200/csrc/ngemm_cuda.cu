@@ -434,7 +434,8 @@ ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, in
 // CTA's 8/16/32 warps split K so that ~32 warps per SM are streaming; a grid K split (atomic
 // wrap-add into a zeroed C) only when even 32 warps per row group are not enough.
 // Skinny kernels' `vec_ok` argument: bit 0 = operands allow 16-byte vector loads, bit 1 = also
-// warm L2 with the CTA's operand rows before the PDL dependency wait (NGEMM_L2_PREFETCH=0 off).
+// warm L2 with the CTA's operand rows before the PDL dependency wait (NGEMM_L2_PREFETCH=0 off),
+// bit 2 = whole in-range chunks take the branch-free load path (NGEMM_SKINNY_FAST=0 off).
 bool l2_prefetch_enabled() {
     static const bool on = [] {
         const char* e = std::getenv("NGEMM_L2_PREFETCH");
@@ -446,7 +447,11 @@ bool l2_prefetch_enabled() {
 int skinny_vec_flags(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, const Batch& bt) {
     const bool vec = reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0;
-    return vec ? (l2_prefetch_enabled() ? 3 : 1) : 0;
+    static const bool fast = [] {
+        const char* e = std::getenv("NGEMM_SKINNY_FAST");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return vec ? (1 | (l2_prefetch_enabled() ? 2 : 0) | (fast ? 4 : 0)) : 0;
 }
 
 template <int MT, int WARPS, int RG = 1>
