@@ -94,7 +94,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                    const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
                    int num_kb_total, TileMap map, int c_mode, const int32_t* __restrict__ guard) {
     // c_mode: 0 = TMA tensor store of C (SWIZZLE_128B staging), 1 = TMA reduce-add into a
-    // zeroed C (split-K), 2 = direct 128-byte row-segment stores (C not TMA-describable).
+    // zeroed C (split-K), 2 = direct scalar stores (C not TMA-describable), 3 = direct 16-byte
+    // vector stores (aligned C, single-wave grids).
     // guard: non-null for a HardwareSaturating call — run only if the operands cannot saturate.
     if (guard != nullptr) {
         pdl_wait();
@@ -183,7 +184,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
-        if (c_mode != 2) tma_prefetch(&tma_c);
+        if (c_mode <= 1) tma_prefetch(&tma_c);
         if (MC == 1 && map.prefetch && guard == nullptr && unit < num_tiles) {
             // warm L2 with this CTA's first STAGES operand slabs before the dependency wait
             // (tma_prefetch_tile_2d: prefetch only, re-read after pdl_wait), so the first HBM
@@ -291,13 +292,14 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(taddr + c, v);
                 tmem_wait_ld();
+                if (t == unit && c == 0 && warp == 4 && lane == 0) TC_TRACE_NOW(10);
                 if (!has_k || row0 >= M) continue;
                 if (map.shift) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] <<= map.shift;  // mod 2^32, like the accumulator
                 }
                 const int col0 = tn * BN + c;
-                if (c_mode != 2) {
+                if (c_mode <= 1) {
                     uint8_t* buf = stage_c + cbuf * S::STAGE_C_BYTES;
                     // the TMA store that last read this buffer must be done with it
                     if (lane == 0) tma_store_wait_read<1>();
@@ -314,17 +316,29 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                         else tma_reduce_add_2d(&tma_c, buf, col0, row0);
                         tma_store_commit();
                     }
+                    if (t == unit && c == 0 && warp == 4 && lane == 0) TC_TRACE_NOW(11);
                     cbuf ^= 1;
                 } else {
+                    // direct stores, lane = row: c_mode 3 (16-byte aligned C) writes each row's
+                    // 128-byte segment with 8 vector stores and never waits on them — for
+                    // single-wave grids, where the TMA store path's staging and drain sit on
+                    // the critical path; c_mode 2 (C not TMA-describable) stores scalars
                     const int64_t row = static_cast<int64_t>(row0) + lane;
                     if (row < M) {
-                        int32_t* crow = C + row * ldc;
+                        int32_t* crow = C + row * ldc + col0;
+                        if (c_mode == 3 && col0 + 32 <= N) {
 #pragma unroll
-                        for (int q = 0; q < 32; ++q)
-                            if (col0 + q < N) crow[col0 + q] = static_cast<int32_t>(v[q]);
+                            for (int j = 0; j < 8; ++j)
+                                st_global_v4(crow + 4 * j, v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                        } else {
+#pragma unroll
+                            for (int q = 0; q < 32; ++q)
+                                if (col0 + q < N) crow[q] = static_cast<int32_t>(v[q]);
+                        }
                     }
                 }
             }
+            if (t == unit && warp == 4 && lane == 0) TC_TRACE_NOW(12);
             tc_fence_before();
             __syncwarp();
             if (lane == 0) {

@@ -29,7 +29,7 @@
 // launch and CTA, %globaltimer stamps of the tcgen05 kernel's phases.  The launch index comes
 // from the host (TileMap::trace_id, one per captured launch), so recording a stamp is a single
 // global store: no loads or atomics that would stall the traced thread.
-constexpr int kTraceL = 64, kTraceCta = 160, kTraceP = 10;
+constexpr int kTraceL = 64, kTraceCta = 160, kTraceP = 16;
 __device__ unsigned long long g_tc_trace[kTraceL][kTraceCta][kTraceP];
 int g_trace_next = 0;  // host: id of the next traced launch
 __device__ __forceinline__ unsigned long long trace_now() {
@@ -703,6 +703,14 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
     return best;
 }
 
+// Epilogue choice for an aligned, unsplit C: the TMA-store epilogue everywhere — direct 16-byte
+// stores from registers (c_mode 3) measured 2-30 % slower even on single-wave grids
+// (profiles/ab_direct_r1.log); NGEMM_TC_DIRECT=1 selects them for experiments.
+bool direct_c_stores(int /*tiles*/, int /*units*/) {
+    const char* e = std::getenv("NGEMM_TC_DIRECT");
+    return e && std::atoi(e) != 0;
+}
+
 // Operand formats and epilogue of one tcgen05 launch: the NGEMM path is u8 x s8 into C; the
 // i16 path issues four launches over byte planes with mixed formats, shifting and adding into C.
 struct TcOps {
@@ -748,6 +756,7 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.trace_id = g_trace_next++;
 #endif
     if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
+    if (c_mode == 0 && map.splits == 1 && !ops.accumulate && direct_c_stores(tiles, units)) c_mode = 3;
     if (ops.accumulate) {
         c_mode = 1;  // C already holds a partial sum: every split reduce-adds into it
     } else if (map.splits > 1) {

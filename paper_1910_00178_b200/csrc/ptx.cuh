@@ -178,6 +178,10 @@ __device__ __forceinline__ uint64_t policy_evict_normal() {
 // Wait until the preceding grid in the stream has completed and its memory is visible (no-op
 // when the kernel was not launched with programmatic stream serialization).
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void st_global_v4(void* p, uint32_t a, uint32_t b, uint32_t c, uint32_t d) {
+    asm volatile("st.global.v4.b32 [%0], {%1, %2, %3, %4};" ::"l"(p), "r"(a), "r"(b), "r"(c), "r"(d) : "memory");
+}
+
 // Warm L2 with global bytes [p, p + bytes) (p 16-byte aligned, bytes a multiple of 16).  Safe to
 // issue BEFORE pdl_wait(): the bytes are only warmed, never consumed — they are re-read after
 // the wait, and L2 is the device's point of coherence, so a line the preceding grid is still

@@ -19,7 +19,7 @@ import numpy as np
 import torch
 
 ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-L_MAX, CTA_MAX, NP = 64, 160, 10
+L_MAX, CTA_MAX, NP = 64, 160, 16
 
 
 def main():
@@ -68,12 +68,14 @@ def main():
             mn = lambda p: np.nanmin(t[L, :, p]) - t0  # noqa: E731
             mx = lambda p: np.nanmax(t[L, :, p]) - t0  # noqa: E731
             gap = np.nanmin(t[L + 1, :, 2]) - np.nanmax(t[L, :, 9])
-            rows.append([mx(0), mx(1), mn(2), mx(2), mn(5), mx(5), mx(6), mn(7), mx(8), mx(9), gap])
+            rows.append([mx(0), mx(1), mn(2), mx(2), mn(5), mx(5), mx(6), mn(7), mx(8), mx(9), gap,
+                         mn(10), mn(11), mn(12)])
         r = np.nanmean(np.array(rows), axis=0) / 1e3
         ctas = int(np.sum(~np.isnan(t[4, :, 0])))
         print(f"{sh:>18s} {us:8.2f} us/launch ({ctas} CTAs) | entry<= {r[0]:.2f} setup<= {r[1]:.2f} "
               f"release {r[2]:.2f}..{r[3]:.2f} data {r[4]:.2f}..{r[5]:.2f} mma-done {r[6]:.2f} "
-              f"epi-first {r[7]:.2f} epi-done {r[8]:.2f} exit {r[9]:.2f} | gap {r[10]:.2f}", flush=True)
+              f"epi-first {r[7]:.2f} epi-done {r[8]:.2f} exit {r[9]:.2f} | gap {r[10]:.2f} | first tile, warp 4: "
+              f"tmem-ld {r[11]:.2f} store0 {r[12]:.2f} tile-stores-issued {r[13]:.2f}", flush=True)
         del a, b, c, g
         torch.cuda.empty_cache()
 

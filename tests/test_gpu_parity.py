@@ -306,14 +306,15 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
     """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64), with and without
     split-K (TMA s32 reduce-add), with TMA-store and direct-store epilogues, vs the oracle."""
     monkeypatch.setenv("NGEMM_TC_CFG", str(cfg))
-    for splits in ("1", "2", "3"):
+    for splits, direct in (("1", "0"), ("1", "1"), ("2", "0"), ("3", "0")):
         monkeypatch.setenv("NGEMM_TC_SPLITS", splits)
+        monkeypatch.setenv("NGEMM_TC_DIRECT", direct)  # TMA-store vs direct vector-store epilogue
         for (m, n, k, ldc) in ((300, 520, 1100, None), (256, 256, 2048, 260), (129, 65, 640, None),
                                (513, 300, 1024, 301), (600, 1024, 700, None), (256, 512, 128, 516)):
             a = oracle.mat_random_u8(m, k, m + cfg)
             b = oracle.mat_random_i8(n, k, n + cfg)
             got = dev_gemm(a, b, EXACT, "tcgen05", ldc=ldc)
-            assert (got == oracle.gemm(a, b, EXACT)).all(), (cfg, splits, m, n, k, ldc)
+            assert (got == oracle.gemm(a, b, EXACT)).all(), (cfg, splits, direct, m, n, k, ldc)
 
 
 @pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
