@@ -48,6 +48,9 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--eager", action="store_true", help="never capture a CUDA graph")
+    p.add_argument("--bdist", default="auto", choices=["auto", "uniform", "normal"],
+                   help="B distribution: uniform int8, or round(N(0, 32)) clipped (config 2's); "
+                        "auto = normal for M <= 16 (config 2), else uniform")
     return p.parse_args()
 
 
@@ -251,7 +254,15 @@ def run_ours(args):
     a_full_rows = torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32)
     a = a_full_rows.to(torch.uint8)
     del a_full_rows
-    b = torch.randint(-128, 128, (N, K), generator=gb, device=dev, dtype=torch.int32).to(torch.int8)
+    bnormal = args.bdist == "normal" or (args.bdist == "auto" and M <= 16)
+
+    def make_b():
+        if bnormal:  # config 2: round(N(0, sigma=32)) clipped to [-128, 127]
+            x = torch.randn((N, K), generator=gb, device=dev, dtype=torch.float32) * 32.0
+            return torch.clamp(torch.round(x), -128, 127).to(torch.int8)
+        return torch.randint(-128, 128, (N, K), generator=gb, device=dev, dtype=torch.int32).to(torch.int8)
+
+    b = make_b()
     c = torch.empty((max(mr, 1), N), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
     picked = _lib.KERNEL_NAMES[kernel] if kernel else api.pick_kernel(max(mr, 1), N, K, mode)
@@ -260,8 +271,7 @@ def run_ours(args):
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     per = (mr * K + N * K + 4 * mr * N)
     nbuf = 1 if per > 2 * l2 else min(64, int((4 * l2) // max(per, 1)) + 1)
-    bs = [b] + [torch.randint(-128, 128, (N, K), generator=gb, device=dev, dtype=torch.int32).to(torch.int8)
-                for _ in range(nbuf - 1)]
+    bs = [b] + [make_b() for _ in range(nbuf - 1)]
     as_ = [a] + [torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32).to(torch.uint8)
                  for _ in range(nbuf - 1)]
     cs = [c] + [torch.empty_like(c) for _ in range(nbuf - 1)]
@@ -382,7 +392,9 @@ def run_ours(args):
             "value": round(value, 2), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 6), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8*s8->s32",
-            "data": "synthetic: A uniform u8 [0,255], B uniform i8 [-128,127] (torch generators seed 0/1, on device)",
+            "data": "synthetic: A uniform u8 [0,255], B " + ("round(N(0,32)) clipped to i8" if bnormal else
+                                                             "uniform i8 [-128,127]") +
+                    " (torch generators seed 0/1, on device)",
             "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode,
                        "sat_semantics": "WideningExact (gemm_ref)" if mode == EXACT else
                        "HardwareSaturating (gemm_sat_oracle)",

@@ -56,78 +56,18 @@ __global__ void repack_kernel(PackedGeom g, const uint8_t* __restrict__ packed, 
 }
 
 // Zeroes C [m x n] (row stride ldc) for a split-K launch — but only when the saturation
-// guard selects the kernel that follows (want_safe = 1: the tensor-core kernel, 0: the
+// guard selects the kernel that follows (want_safe = GUARD_TC: the tensor-core kernel, GUARD_SIMT: the
 // CUDA-core one), so the path that does not run never clobbers the other's result.
 __global__ void guarded_zero_kernel(int32_t* __restrict__ c, int64_t ldc, int64_t m, int64_t n,
                                     const int32_t* __restrict__ guard, int want_safe) {
     pdl_launch_dependents();
     pdl_wait();
-    if (sat_safe(guard) != want_safe) return;
+    if (!guard_runs(guard, want_safe)) return;
     const int64_t total = m * n;
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t r = i / n;
         c[r * ldc + (i - r * n)] = 0;
-    }
-}
-
-// Operand ranges for the saturation-safety proof of the dispatcher: out = {max A, max B, -min B}
-// (out zeroed by the caller).  Rows are scanned in 16-byte chunks with packed-byte SIMD
-// (__vmaxu4 / __vmaxs4 / __vmins4) when aligned; one atomicMax per warp.
-__global__ void operand_range_kernel(const uint8_t* __restrict__ a, int64_t lda, int64_t m,
-                                     const int8_t* __restrict__ b, int64_t ldb, int64_t n, int64_t k, int vec_ok,
-                                     int32_t* __restrict__ out) {
-    pdl_launch_dependents();
-    pdl_wait();
-    uint32_t amax4 = 0, bmax4 = 0x80808080u, bmin4 = 0x7F7F7F7Fu;
-    const int64_t cpr = (k + 15) / 16;  // 16-byte chunks per row
-    const int64_t ta = m * cpr, total = ta + n * cpr;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const bool is_a = i < ta;
-        const int64_t j = is_a ? i : i - ta;
-        const int64_t r = j / cpr, c0 = (j - r * cpr) * 16;
-        const uint8_t* p = is_a ? a + r * lda + c0 : reinterpret_cast<const uint8_t*>(b) + r * ldb + c0;
-        uint32_t w[4];
-        if (vec_ok && c0 + 16 <= k) {
-            const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
-            w[0] = v.x; w[1] = v.y; w[2] = v.z; w[3] = v.w;
-        } else {
-            // pad with a neutral byte: 0 for A (u8 max), B's own first byte for B (signed max/min)
-            const uint32_t pad = is_a ? 0u : static_cast<uint32_t>(p[0]);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) w[q] = pad * 0x01010101u;
-#pragma unroll
-            for (int t = 0; t < 16; ++t)
-                if (c0 + t < k) w[t >> 2] = (w[t >> 2] & ~(0xFFu << (8 * (t & 3)))) | (static_cast<uint32_t>(p[t]) << (8 * (t & 3)));
-        }
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (is_a) amax4 = __vmaxu4(amax4, w[q]);
-            else {
-                bmax4 = __vmaxs4(bmax4, w[q]);
-                bmin4 = __vmins4(bmin4, w[q]);
-            }
-        }
-    }
-    int32_t amax = 0, bmax = -128, bmin = 127;
-#pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        amax = max(amax, static_cast<int32_t>((amax4 >> (8 * q)) & 0xFF));
-        bmax = max(bmax, static_cast<int32_t>(static_cast<int8_t>((bmax4 >> (8 * q)) & 0xFF)));
-        bmin = min(bmin, static_cast<int32_t>(static_cast<int8_t>((bmin4 >> (8 * q)) & 0xFF)));
-    }
-    int32_t bneg = max(0, -bmin);
-    bmax = max(0, bmax);
-    for (int o = 16; o > 0; o >>= 1) {
-        amax = max(amax, __shfl_xor_sync(0xffffffffu, amax, o));
-        bmax = max(bmax, __shfl_xor_sync(0xffffffffu, bmax, o));
-        bneg = max(bneg, __shfl_xor_sync(0xffffffffu, bneg, o));
-    }
-    if ((threadIdx.x & 31) == 0) {
-        atomicMax(&out[0], amax);
-        atomicMax(&out[1], bmax);
-        atomicMax(&out[2], bneg);
     }
 }
 

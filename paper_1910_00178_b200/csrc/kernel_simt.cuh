@@ -56,9 +56,11 @@ __global__ void __launch_bounds__(simt::THREADS, 2)
     constexpr int TT = TILE / 16;     // outputs per thread per dimension
     constexpr int LDS = TILE + 4;     // padded word stride (bank-conflict free stores)
     constexpr int LOADS = (TILE * 2 + THREADS - 1) / THREADS;  // uint4 loads per operand per thread
-    pdl_launch_dependents();
+    // On the guarded saturating chain the next grids launch as this one's CTAs exit: early
+    // dependents would hold SM slots the dense kernel needs when it is the one selected.
+    if (guard == nullptr) pdl_launch_dependents();
     pdl_wait();
-    if (guard != nullptr && sat_safe(guard)) return;  // the tensor-core kernel took this call
+    if (guard != nullptr && !guard_runs(guard, GUARD_SIMT)) return;  // the tensor cores took this call
     __shared__ __align__(16) uint32_t As[BKW][LDS];
     __shared__ __align__(16) uint32_t Bs[BKW][LDS];
 

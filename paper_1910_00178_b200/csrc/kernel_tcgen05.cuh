@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     // guard: non-null for a HardwareSaturating call — run only if the operands cannot saturate.
     if (guard != nullptr) {
         pdl_wait();
-        if (!sat_safe(guard)) return;  // uniform across the grid (and across a CTA pair)
+        if (!guard_runs(guard, GUARD_TC)) return;  // uniform across the grid (and across a CTA pair)
     }
     TC_TRACE_KEEP(0);
     using S = tc::Smem<BN, STAGES, CG>;

@@ -53,6 +53,7 @@ __device__ __forceinline__ void trace_put(int L, int p, unsigned long long t) {
 #endif
 
 #include "kernel_layout.cuh"
+#include "kernel_satfix.cuh"
 #include "kernel_simt.cuh"
 #include "kernel_skinny.cuh"
 #include "kernel_tcgen05.cuh"
@@ -827,31 +828,104 @@ cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int
     return cudaMemcpy2DAsync(dst, kp, src, k, k, rows, cudaMemcpyHostToDevice, st);
 }
 
-// HardwareSaturating with a device-side proof: one pass computes the operand ranges; if no
-// int16 pair sum can leave [-32768, 32767] the exact tensor-core kernel runs (identical result),
-// otherwise the CUDA-core saturating kernel does — both are enqueued, each exits immediately
-// unless the proof selects it, so the stream never synchronises with the host.
-constexpr double kSatProofMinWork = 1 << 24;
+// HardwareSaturating for M > 16 without a host round trip (kernel_satfix.cuh):
+//   1. sat_prep_a_kernel: max A -> guard[0], A in the fix kernel's pair-major tile layout
+//   2. sat_prep_b_kernel: B_safe = B with the pairs that could clamp zeroed, B's tiles, the
+//      dangerous-pair masks, per-tile counts, the total count and the hybrid threshold
+//                                                               -> guard[4..7]
+//   3. the dense CUDA-core kernel on (A, B)    runs when more than sat_hybrid_max_frac() of
+//      the pairs are dangerous (extreme inputs: the sparse fix would cost more) (selection 2)
+//   4. tcgen05 on (A, B_safe)                  runs when the selection is 0 or 1
+//   5. sat_fix_kernel adds the clamped sums of the dangerous pairs       (selection 1)
+// Every launch is enqueued; each reads the guard after griddepcontrol.wait and exits unless
+// selected, so the stream never synchronises with the host.
+// Used for M >= 256 and >= 2^29 MACs: below that the chain's fixed cost (five launches, ~25 us)
+// loses to the dense kernel even on the sparsest inputs (profiles/sweep_sat_hybrid_r1.log).
+// Above it, the break-even dangerous fraction (uniform vs sigma-32 B against the dense kernel)
+// grows with the work: ~0.04 at 0.5 G MACs, 0.36-0.47 at 1 G, 0.44-0.50 at 2 G, 0.54-0.59 at
+// 8-69 G.  NGEMM_SAT_HYBRID=1 forces the chain (tests), 0 disables it.
+constexpr int64_t kSatHybridMinM = 256;
+constexpr double kSatHybridMinWork = static_cast<double>(1ll << 29);
+double sat_hybrid_max_frac(int64_t m, int64_t n, int64_t k) {
+    const double w = static_cast<double>(m) * n * k;
+    return w < 1e9 ? 0.03 : w < 2e9 ? 0.35 : w < 8e9 ? 0.44 : 0.54;
+}
+int sat_hybrid_env() {
+    const char* e = std::getenv("NGEMM_SAT_HYBRID");
+    return e ? std::atoi(e) : -1;
+}
 
-ngemm_status launch_sat_proved(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
+ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                                int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
-    int32_t* range = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&range), 16, st));
-    ngemm_status s = NGEMM_OK;
-    if (cudaMemsetAsync(range, 0, 16, st) != cudaSuccess) s = fail(NGEMM_ERR_CUDA, "memset(range) failed");
+    using namespace satfix;
+    const int64_t chunks = (k + CHUNK - 1) / CHUNK;
+    const int64_t lds = chunks * CHUNK;  // B_safe pitch (TMA-describable, zero past k)
+    const int64_t tn = (n + TN - 1) / TN, tm = (m + TM - 1) / TM;
+    // one allocation: guard | flags (both zeroed) | L_t | A_pm | B_t | B_safe
+    const size_t guard_b = 64, flags_b = round_up(static_cast<int64_t>(tn * chunks * 4), 256);
+    const size_t lt_off = guard_b + flags_b, lt_b = static_cast<size_t>(tn * chunks) * L_TILE;
+    const size_t apm_off = round_up(static_cast<int64_t>(lt_off + lt_b), 256), apm_b = static_cast<size_t>(tm * chunks) * A_TILE;
+    const size_t bt_off = apm_off + apm_b, bt_b = static_cast<size_t>(tn * chunks) * B_TILE;
+    const size_t bs_off = bt_off + bt_b, bs_b = static_cast<size_t>(n * lds);
+    CUtensorMap tcm;
+    ngemm_status s = make_tmap_c(&tcm, c, m, n, ldc);
+    if (s != NGEMM_OK) return s;
+    uint8_t* buf = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), bs_off + bs_b, st));
+    int32_t* guard = reinterpret_cast<int32_t*>(buf);
+    uint32_t* flags = reinterpret_cast<uint32_t*>(buf + guard_b);
+    uint8_t* lt = buf + lt_off;
+    uint32_t* apm = reinterpret_cast<uint32_t*>(buf + apm_off);
+    uint8_t* bt = buf + bt_off;
+    uint8_t* bsafe = buf + bs_off;
+    if (cudaMemsetAsync(buf, 0, guard_b + flags_b, st) != cudaSuccess) s = fail(NGEMM_ERR_CUDA, "memset(guard) failed");
+    const int va = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0);
+    const int vb = (reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0);
+    auto launched = [&](cudaError_t e) {
+        if (e != cudaSuccess) return fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+        g_launches.fetch_add(1, std::memory_order_relaxed);
+        return NGEMM_OK;
+    };
+    auto grid_for = [&](int64_t items) {
+        return dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, di.sms * 16))));
+    };
+    if (s == NGEMM_OK)
+        s = launched(launch_k(sat_prep_a_kernel, grid_for(tm * chunks * 8 * (TM / 2)), dim3(256), 0, st, 1, 1, a, lda,
+                              m, k, va, chunks, apm, guard));
     if (s == NGEMM_OK) {
-        const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
-                            lda % 16 == 0 && ldb % 16 == 0);
-        const int64_t chunks = (m + n) * ((k + 15) / 16);
-        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((chunks + 255) / 256, di.sms * 8));
-        cudaError_t e = launch_k(operand_range_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, a,
-                                 lda, m, b, ldb, n, k, vec_ok, range);
-        if (e != cudaSuccess) s = fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
-        else g_launches.fetch_add(1, std::memory_order_relaxed);
+        const unsigned long long thresh =
+            static_cast<unsigned long long>(sat_hybrid_max_frac(m, n, k) * static_cast<double>(n) *
+                                            static_cast<double>((k + 1) / 2));
+        s = launched(launch_k(sat_prep_b_kernel, grid_for(tn * chunks * TN * 4), dim3(256), 0, st, 1, 1, b, ldb, n, k,
+                              vb, chunks, bsafe, lds, bt, lt, flags, guard, thresh));
     }
-    if (s == NGEMM_OK) s = launch_tcgen05(a, lda, b, ldb, c, ldc, m, n, k, di, st, range);
-    if (s == NGEMM_OK) s = launch_simt(a, lda, b, ldb, c, ldc, m, n, k, NGEMM_SAT_HARDWARE, st, range);
-    cudaFreeAsync(range, st);
+    // the dense kernel first: when not selected its CTAs exit at once, and when selected the
+    // tensor-core and fix grids behind it exit at once
+    if (s == NGEMM_OK) s = launch_simt(a, lda, b, ldb, c, ldc, m, n, k, NGEMM_SAT_HARDWARE, st, guard);
+    if (s == NGEMM_OK) s = launch_tcgen05(a, lda, reinterpret_cast<const int8_t*>(bsafe), lds, c, ldc, m, n, k, di, st, guard);
+    if (s == NGEMM_OK) {
+        static std::once_flag once[64];
+        int dev = 0;
+        cudaGetDevice(&dev);
+        std::call_once(once[dev & 63], [&] { s = set_smem(sat_fix_kernel, SMEM); });
+    }
+    if (s == NGEMM_OK) {
+        // one CTA per SM: ~3 waves of CTAs for balance (the TMA reduce-add epilogue makes K
+        // splits cheap), >= 2 chunks per CTA when that still fills every SM so the two-stage
+        // pipeline overlaps loads with math
+        const int64_t tiles = tn * tm;
+        int64_t splits = std::max<int64_t>(1, std::min<int64_t>(chunks, (3 * di.sms + tiles - 1) / tiles));
+        if (tiles * (chunks / 2) >= di.sms) splits = std::min<int64_t>(splits, std::max<int64_t>(1, chunks / 2));
+        splits = std::max<int64_t>(splits, (chunks + MAX_LIST - 1) / MAX_LIST);  // the CTA's chunk list fits
+        const int64_t per = (chunks + splits - 1) / splits;
+        splits = (chunks + per - 1) / per;
+        dim3 grid(static_cast<unsigned>(tn), static_cast<unsigned>(tm), static_cast<unsigned>(splits));
+        if (tm > 65535 || splits > 65535) s = fail(NGEMM_ERR_SHAPE, "sat fix: M or K too large");
+        else
+            s = launched(launch_k(sat_fix_kernel, grid, dim3(THREADS), SMEM, st, 1, 1, tcm, apm, bt, lt, flags, chunks,
+                                  per, guard));
+    }
+    cudaFreeAsync(buf, st);
     return s;
 }
 
@@ -887,8 +961,11 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
     if (s != NGEMM_OK) return s;
     if (kernel == NGEMM_KERNEL_AUTO) kernel = pick(m, n, k, mode);
     if (kernel == NGEMM_KERNEL_SIMT && mode == NGEMM_SAT_HARDWARE && auto_kernel && m > kSkinnyMaxM &&
-        static_cast<double>(m) * n * k >= kSatProofMinWork)
-        return launch_sat_proved(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+        reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0) {  // the fix adds into C by TMA reduce
+        const int env = sat_hybrid_env();
+        const bool big = m >= kSatHybridMinM && static_cast<double>(m) * n * k >= kSatHybridMinWork;
+        if (env == 1 || (env != 0 && big)) return launch_sat_hybrid(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    }
     switch (kernel) {
     case NGEMM_KERNEL_SIMT: return launch_simt(a, lda, b, ldb, c, ldc, m, n, k, mode, st);
     case NGEMM_KERNEL_SKINNY: return launch_skinny(a, lda, b, ldb, c, ldc, m, n, k, mode, di, st);
@@ -1633,7 +1710,7 @@ ngemm_status ngemm_cuda_tune(int64_t m, int64_t n, int64_t k, int sat_mode, int 
         c.kernel = NGEMM_KERNEL_SIMT;
         cands.push_back(c);
         if (sat_mode != NGEMM_SAT_EXACT && m > kSkinnyMaxM) {
-            Choice p;  // the range-proof dispatcher (tensor cores when inputs cannot saturate)
+            Choice p;  // the hybrid dispatcher (tensor cores + sparse fix of the pairs that can clamp)
             p.kernel = NGEMM_KERNEL_AUTO;
             cands.push_back(p);
         }

@@ -55,6 +55,28 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// ---------------------------------------------------------------- shared-window loads
+__device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
+    uint4 v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u16(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u16 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+    uint16_t v;
+    asm volatile("ld.shared.u8 %0, [%1];" : "=h"(v) : "r"(addr));
+    return v;
+}
+
 // ---------------------------------------------------------------- mbarrier
 __device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
@@ -97,6 +119,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 }
 
 // ---------------------------------------------------------------- TMA
+// 1-D bulk copy global -> shared completing on an mbarrier (16-byte aligned, size % 16 == 0).
+__device__ __forceinline__ void bulk_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     smem_u32(dst)),
+                 "l"(src), "r"(bytes), "r"(smem_u32(bar))
+                 : "memory");
+}
 __device__ __forceinline__ void tma_prefetch(const CUtensorMap* map) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
 }
@@ -199,13 +228,26 @@ __device__ __forceinline__ void tma_prefetch_tile_2d(const CUtensorMap* map, int
 // Let the dependent grid start launching (its CTAs run their prologue, then pdl_wait()).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// ---------------------------------------------------------------- saturation-safety guard
-// range = {max a (u8), max b, -min b} written by operand_range_kernel.  Every pair sum
-// a0*b0 + a1*b1 then lies in [-2*amax*bneg, 2*amax*bmax]; when that fits int16 the
-// HardwareSaturating result equals the exact one and the tensor cores may compute it.
-__device__ __forceinline__ int sat_safe(const int32_t* range) {
-    const int64_t amax = range[0], bmax = range[1], bneg = range[2];
-    return (2 * amax * bmax <= 32767 && 2 * amax * bneg <= 32768) ? 1 : 0;
+// ---------------------------------------------------------------- saturation guard
+// The HardwareSaturating dispatcher's device-side decision, so the stream never synchronises
+// with the host (kernel_satfix.cuh).  guard (int32[16], zeroed by the host):
+//   [0]    = max a (u8)                             written by sat_prep_a_kernel
+//   [4..5] = u64 number of "dangerous" B pairs      written by sat_prep_b_kernel
+//   [6..7] = u64 threshold for the hybrid path      written by sat_prep_b_kernel
+// A pair (b0, b1) is dangerous when some a0, a1 in [0, max a] can push a0*b0 + a1*b1 out of
+// int16; every other pair's sum is exact, so those pairs can go to the tensor cores.
+// Selection: 0 = no dangerous pair (tensor cores alone), 1 = tensor cores on B with the
+// dangerous pairs zeroed + the CUDA-core fix of the dangerous pairs, 2 = dense CUDA-core kernel.
+__device__ __forceinline__ int sat_select(const int32_t* guard) {
+    const unsigned long long cnt = *reinterpret_cast<const volatile unsigned long long*>(guard + 4);
+    const unsigned long long thr = *reinterpret_cast<const volatile unsigned long long*>(guard + 6);
+    return cnt == 0 ? 0 : (cnt <= thr ? 1 : 2);
+}
+enum GuardRole { GUARD_SIMT = 0, GUARD_TC = 1, GUARD_FIX = 2 };
+// Whether the launch with this role runs under the guard's selection.
+__device__ __forceinline__ bool guard_runs(const int32_t* guard, int role) {
+    const int sel = sat_select(guard);
+    return role == GUARD_TC ? sel <= 1 : (role == GUARD_FIX ? sel == 1 : sel == 2);
 }
 
 // ---------------------------------------------------------------- cluster / DSMEM

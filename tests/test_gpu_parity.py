@@ -321,7 +321,7 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
 def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
     """Skinny (M <= 16) variants: 0 warp-butterfly dp4a, 1 lanes-own-rows dp4a (broadcast A),
     2 tensor-core swap-AB, 3 warp-MMA load stream (2 and 3: exact mode only; sat falls back
-    to 1) — all bit-exact."""
+    to 1), 4 dp4a load stream (sat) — all bit-exact."""
     monkeypatch.setenv("NGEMM_SKINNY_VARIANT", variant)
     for c in golden["config2"]:
         a = oracle.mat_random_u8(c["m"], c["k"], 0)
@@ -357,6 +357,50 @@ def test_sat_mode_on_provably_safe_inputs(cuda, oracle):
     got = dev_gemm(a, b, SAT, "auto")
     assert (got == oracle.gemm(a, b, SAT)).all()
     assert (got != oracle.gemm(a, b, EXACT)).any()
+
+
+def _normal_i8(rng, shape, sigma=32.0):
+    return np.clip(np.rint(rng.normal(0.0, sigma, shape)), -128, 127).astype(np.int8)
+
+
+@pytest.mark.parametrize("case", ["uniform", "normal", "extreme", "dense_frac", "sparse_edges", "safe_b"])
+def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
+    """HardwareSaturating for M > 16 (kernel_satfix.cuh): tcgen05 on B with the pairs that could
+    clamp zeroed, plus the CUDA-core fix of those pairs — or the dense CUDA-core kernel when more
+    than 60 % of the pairs could clamp.  Every selection, ragged shapes (odd K, K < 256, K not a
+    multiple of 16, unaligned leading dimensions) must equal gemm_sat_oracle bit for bit."""
+    rng = np.random.default_rng(["uniform", "normal", "extreme", "dense_frac", "sparse_edges", "safe_b"].index(case))
+    # NGEMM_SAT_HYBRID=1 forces the chain below its size threshold (M >= 256, >= 2^29 MACs);
+    # 1000^3 and 512 x 1280 x 1024 take it by default
+    monkeypatch.setenv("NGEMM_SAT_HYBRID", "1")
+    shapes = [(300, 333, 777), (257, 390, 200), (40, 640, 1024), (129, 4100, 100), (1000, 1000, 1000),
+              (512, 1280, 1024)]
+    for (m, n, k) in shapes:
+        a = rng.integers(0, 256, (m, k), dtype=np.uint8)
+        if case == "uniform":
+            b = rng.integers(-128, 128, (n, k), dtype=np.int8)
+        elif case == "normal":
+            b = _normal_i8(rng, (n, k))
+        elif case == "extreme":
+            a[:] = 255
+            b = np.full((n, k), 127, np.int8)
+            b[::3] = -128
+        elif case == "dense_frac":  # ~70 % of the pairs dangerous: the dense kernel runs
+            b = np.where(rng.random((n, k)) < 0.84, 127, rng.integers(-128, 128, (n, k))).astype(np.int8)
+        elif case == "sparse_edges":  # a few dangerous pairs at chunk edges and in the odd-K tail
+            b = rng.integers(-50, 51, (n, k), dtype=np.int8)
+            for (r, c) in ((0, 0), (n - 1, k - 1), (n // 2, min(254, k - 1)), (n // 2, min(255, k - 1)),
+                           (n // 3, min(256, k - 1)), (1, k - 2)):
+                b[r, c] = 127 if (r + c) % 2 else -128
+                b[r, c ^ 1 if (c ^ 1) < k else c] = 127 if (r + c) % 2 else -128
+        else:  # safe_b: no pair can clamp although A spans [0, 255]
+            b = rng.integers(-64, 65, (n, k), dtype=np.int8)
+        ref = oracle.gemm(a, b, SAT)
+        got = dev_gemm(a, b, SAT, "auto")
+        assert (got == ref).all(), (case, m, n, k, int((got != ref).sum()))
+        if (m, n, k) == (300, 333, 777):  # ragged leading dimensions (no 16-byte vector loads)
+            got = dev_gemm(a, b, SAT, "auto", lda=k + 3, ldb=k + 5, ldc=n + 1)
+            assert (got == ref).all(), (case, "ld", int((got != ref).sum()))
 
 
 def test_host_entry_pipelined_pinned(cuda, oracle):
