@@ -60,8 +60,8 @@ typedef enum {
 /* Kernel selection; AUTO is what every reference-facing entry uses. */
 typedef enum {
     NGEMM_KERNEL_AUTO = 0,
-    NGEMM_KERNEL_TCGEN05 = 1, /* tensor-core tcgen05.mma kind::i8 (exact mode; sat mode only when
-                                 the inputs provably cannot saturate) */
+    NGEMM_KERNEL_TCGEN05 = 1, /* tensor-core tcgen05.mma kind::i8 (exact mode only; AUTO runs the
+                                 saturating mode on it too, for the pairs that cannot clamp) */
     NGEMM_KERNEL_SIMT = 2,    /* CUDA-core dp4a tiled kernel, both modes (the Engine::Emulated path) */
     NGEMM_KERNEL_SKINNY = 3   /* memory-bound M <= 16 path, both modes */
 } ngemm_kernel;
