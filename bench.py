@@ -48,9 +48,12 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--eager", action="store_true", help="never capture a CUDA graph")
-    p.add_argument("--bdist", default="auto", choices=["auto", "uniform", "normal"],
+    p.add_argument("--bdist", default="auto", choices=["auto", "uniform", "normal", "max", "min"],
                    help="B distribution: uniform int8, or round(N(0, 32)) clipped (config 2's); "
-                        "auto = normal for M <= 16 (config 2), else uniform")
+                        "auto = normal for M <= 16 (config 2), else uniform; max / min = all 127 / "
+                        "all -128 (config 4's extremes)")
+    p.add_argument("--adist", default="uniform", choices=["uniform", "max"],
+                   help="A distribution: uniform u8, or all 255 (config 4's extreme)")
     return p.parse_args()
 
 
@@ -251,12 +254,21 @@ def run_ours(args):
     # synthetic inputs with the config's distributions, generated on the device
     ga = torch.Generator(device=dev).manual_seed(0)
     gb = torch.Generator(device=dev).manual_seed(1)
-    a_full_rows = torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32)
-    a = a_full_rows.to(torch.uint8)
-    del a_full_rows
+    def make_a():
+        if args.adist == "max":  # config 4: all 255
+            return torch.full((max(mr, 1), K), 255, device=dev, dtype=torch.uint8)
+        return torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32).to(torch.uint8)
+
+    a = make_a()
     bnormal = args.bdist == "normal" or (args.bdist == "auto" and M <= 16)
+    b_desc = ("all %d" % (127 if args.bdist == "max" else -128) if args.bdist in ("max", "min") else
+              "round(N(0,32)) clipped to i8" if bnormal else "uniform i8 [-128,127]")
+    data_desc = ("synthetic: A " + ("all 255" if args.adist == "max" else "uniform u8 [0,255]") + ", B " + b_desc +
+                 " (torch generators seed 0/1, on device)")
 
     def make_b():
+        if args.bdist in ("max", "min"):  # config 4's extremes
+            return torch.full((N, K), 127 if args.bdist == "max" else -128, device=dev, dtype=torch.int8)
         if bnormal:  # config 2: round(N(0, sigma=32)) clipped to [-128, 127]
             x = torch.randn((N, K), generator=gb, device=dev, dtype=torch.float32) * 32.0
             return torch.clamp(torch.round(x), -128, 127).to(torch.int8)
@@ -272,8 +284,7 @@ def run_ours(args):
     per = (mr * K + N * K + 4 * mr * N)
     nbuf = 1 if per > 2 * l2 else min(64, int((4 * l2) // max(per, 1)) + 1)
     bs = [b] + [make_b() for _ in range(nbuf - 1)]
-    as_ = [a] + [torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32).to(torch.uint8)
-                 for _ in range(nbuf - 1)]
+    as_ = [a] + [make_a() for _ in range(nbuf - 1)]
     cs = [c] + [torch.empty_like(c) for _ in range(nbuf - 1)]
 
     def step(i):
@@ -392,9 +403,7 @@ def run_ours(args):
             "value": round(value, 2), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 6), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8*s8->s32",
-            "data": "synthetic: A uniform u8 [0,255], B " + ("round(N(0,32)) clipped to i8" if bnormal else
-                                                             "uniform i8 [-128,127]") +
-                    " (torch generators seed 0/1, on device)",
+            "data": data_desc,
             "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode,
                        "sat_semantics": "WideningExact (gemm_ref)" if mode == EXACT else
                        "HardwareSaturating (gemm_sat_oracle)",

@@ -55,22 +55,6 @@ __global__ void repack_kernel(PackedGeom g, const uint8_t* __restrict__ packed, 
     }
 }
 
-// Zeroes C [m x n] (row stride ldc) for a split-K launch — but only when the saturation
-// guard selects the kernel that follows (want_safe = GUARD_TC: the tensor-core kernel, GUARD_SIMT: the
-// CUDA-core one), so the path that does not run never clobbers the other's result.
-__global__ void guarded_zero_kernel(int32_t* __restrict__ c, int64_t ldc, int64_t m, int64_t n,
-                                    const int32_t* __restrict__ guard, int want_safe) {
-    pdl_launch_dependents();
-    pdl_wait();
-    if (!guard_runs(guard, want_safe)) return;
-    const int64_t total = m * n;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int64_t r = i / n;
-        c[r * ldc + (i - r * n)] = 0;
-    }
-}
-
 // Deterministic full-range operand fill for the tuner (splitmix64 of the element index).
 __global__ void fill_random_kernel(uint8_t* __restrict__ p, int64_t rows, int64_t cols, int64_t ld, uint64_t seed) {
     const int64_t total = rows * cols;

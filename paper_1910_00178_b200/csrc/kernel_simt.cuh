@@ -51,16 +51,13 @@ template <int MODE, int TILE>
 __global__ void __launch_bounds__(simt::THREADS, 2)
     simt_gemm_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                      int32_t* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int vec_ok,
-                     int c_vec_ok, const int32_t* __restrict__ guard, int64_t k_split, int accumulate) {
+                     int c_vec_ok, int64_t k_split, int accumulate) {
     using namespace simt;
     constexpr int TT = TILE / 16;     // outputs per thread per dimension
     constexpr int LDS = TILE + 4;     // padded word stride (bank-conflict free stores)
     constexpr int LOADS = (TILE * 2 + THREADS - 1) / THREADS;  // uint4 loads per operand per thread
-    // On the guarded saturating chain the next grids launch as this one's CTAs exit: early
-    // dependents would hold SM slots the dense kernel needs when it is the one selected.
-    if (guard == nullptr) pdl_launch_dependents();
+    pdl_launch_dependents();
     pdl_wait();
-    if (guard != nullptr && !guard_runs(guard, GUARD_SIMT)) return;  // the tensor cores took this call
     __shared__ __align__(16) uint32_t As[BKW][LDS];
     __shared__ __align__(16) uint32_t Bs[BKW][LDS];
 

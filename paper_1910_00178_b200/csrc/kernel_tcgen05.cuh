@@ -92,15 +92,10 @@ template <int BN, int STAGES, int CG, int MC = 1>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
                    const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
-                   int num_kb_total, TileMap map, int c_mode, const int32_t* __restrict__ guard) {
+                   int num_kb_total, TileMap map, int c_mode) {
     // c_mode: 0 = TMA tensor store of C (SWIZZLE_128B staging), 1 = TMA reduce-add into a
     // zeroed C (split-K), 2 = direct scalar stores (C not TMA-describable), 3 = direct 16-byte
     // vector stores (aligned C, single-wave grids).
-    // guard: non-null for a HardwareSaturating call — run only if the operands cannot saturate.
-    if (guard != nullptr) {
-        pdl_wait();
-        if (!guard_runs(guard, GUARD_TC)) return;  // uniform across the grid (and across a CTA pair)
-    }
     TC_TRACE_KEEP(0);
     using S = tc::Smem<BN, STAGES, CG>;
     constexpr int UMMA_M = tc::BM * CG;
@@ -185,7 +180,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
         if (c_mode <= 1) tma_prefetch(&tma_c);
-        if (MC == 1 && map.prefetch && guard == nullptr && unit < num_tiles) {
+        if (MC == 1 && map.prefetch && unit < num_tiles) {
             // warm L2 with this CTA's first STAGES operand slabs before the dependency wait
             // (tma_prefetch_tile_2d: prefetch only, re-read after pdl_wait), so the first HBM
             // round trips overlap the preceding grid's tail and this CTA's setup

@@ -260,18 +260,10 @@ ngemm_status set_smem(K kernel, int bytes) {
     return NGEMM_OK;
 }
 
-// Zero C before a split-K launch: a plain memset, or — on the guarded saturating path — a
-// kernel that only zeroes when the guard selects the launch that follows.
-ngemm_status zero_c(int32_t* c, int64_t ldc, int64_t m, int64_t n, const int32_t* guard, int want_safe,
-                    const DevInfo& di, cudaStream_t st) {
-    if (guard == nullptr) {
-        if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
-        else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
-        return NGEMM_OK;
-    }
-    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((m * n + 255) / 256, di.sms * 4));
-    NG_LAUNCH(guarded_zero_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, c, ldc, m, n, guard,
-              want_safe);
+// Zero C before a split-K launch (the partial sums are wrap-added into it).
+ngemm_status zero_c(int32_t* c, int64_t ldc, int64_t m, int64_t n, cudaStream_t st) {
+    if (ldc == n) NG_CUDA(cudaMemsetAsync(c, 0, static_cast<size_t>(m * n) * 4, st));
+    else NG_CUDA(cudaMemset2DAsync(c, static_cast<size_t>(ldc) * 4, 0, static_cast<size_t>(n) * 4, m, st));
     return NGEMM_OK;
 }
 
@@ -279,8 +271,7 @@ ngemm_status zero_c(int32_t* c, int64_t ldc, int64_t m, int64_t n, const int32_t
 // plus K splits (32-byte aligned) so that ~2 CTAs per SM are busy.  kbytes/lda/ldb in bytes.
 template <int MODE>
 ngemm_status launch_simt_bytes(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
-                               int64_t m, int64_t n, int64_t kbytes, const DevInfo& di, cudaStream_t st,
-                               const int32_t* guard) {
+                               int64_t m, int64_t n, int64_t kbytes, const DevInfo& di, cudaStream_t st) {
     const int vec_ok = (reinterpret_cast<uintptr_t>(a) % 16 == 0 && reinterpret_cast<uintptr_t>(b) % 16 == 0 &&
                         lda % 16 == 0 && ldb % 16 == 0);
     const int c_vec = (reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0);
@@ -290,7 +281,7 @@ ngemm_status launch_simt_bytes(const uint8_t* a, int64_t lda, const int8_t* b, i
         dim3 grid(static_cast<unsigned>((n + 127) / 128), static_cast<unsigned>((m + 127) / 128), 1);
         if (grid.y > 65535) return fail(NGEMM_ERR_SHAPE, "simt: M too large");
         NG_LAUNCH(simt_gemm_kernel<MODE, 128>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n,
-                  kbytes, vec_ok, c_vec, guard, kbytes, 0);
+                  kbytes, vec_ok, c_vec, kbytes, 0);
         return NGEMM_OK;
     }
     const int64_t tiles64 = ((m + 63) / 64) * ((n + 63) / 64);
@@ -298,22 +289,22 @@ ngemm_status launch_simt_bytes(const uint8_t* a, int64_t lda, const int8_t* b, i
     const int64_t k_split = round_up((kbytes + splits - 1) / splits, 32);
     splits = (kbytes + k_split - 1) / k_split;
     if (splits > 1) {
-        ngemm_status zs = zero_c(c, ldc, m, n, guard, 0, di, st);
+        ngemm_status zs = zero_c(c, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
     dim3 grid(static_cast<unsigned>((n + 63) / 64), static_cast<unsigned>((m + 63) / 64), static_cast<unsigned>(splits));
     NG_LAUNCH(simt_gemm_kernel<MODE, 64>, grid, dim3(simt::THREADS), 0, st, 1, 1, a, lda, b, ldb, c, ldc, m, n, kbytes,
-              vec_ok, c_vec, guard, k_split, splits > 1 ? 1 : 0);
+              vec_ok, c_vec, k_split, splits > 1 ? 1 : 0);
     return NGEMM_OK;
 }
 
 ngemm_status launch_simt(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
-                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st, const int32_t* guard = nullptr) {
+                         int64_t m, int64_t n, int64_t k, int mode, cudaStream_t st) {
     int dev = 0;
     cudaGetDevice(&dev);
     const DevInfo di = dev_info(dev);
-    return mode == NGEMM_SAT_EXACT ? launch_simt_bytes<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st, guard)
-                                   : launch_simt_bytes<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st, guard);
+    return mode == NGEMM_SAT_EXACT ? launch_simt_bytes<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
+                                   : launch_simt_bytes<0>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
 }
 
 // i16 x i16 -> i32 (the reference's 16-bit path, gemm.hpp:161-190, 245-281): SIMT kernel in
@@ -323,7 +314,7 @@ ngemm_status launch_simt_i16(const int16_t* a, int64_t lda, const int16_t* b, in
     int dev = 0;
     cudaGetDevice(&dev);
     return launch_simt_bytes<2>(reinterpret_cast<const uint8_t*>(a), lda * 2, reinterpret_cast<const int8_t*>(b),
-                                ldb * 2, c, ldc, m, n, k * 2, dev_info(dev), st, nullptr);
+                                ldb * 2, c, ldc, m, n, k * 2, dev_info(dev), st);
 }
 
 constexpr int kSkinnyMaxM = 16;
@@ -463,7 +454,7 @@ ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b,
     const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
     splits = (k + k_range - 1) / k_range;
     for (int z = 0; z < bt.count && splits > 1; ++z) {
-        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, nullptr, 0, di, st);
+        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
@@ -520,7 +511,7 @@ ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b,
     const int64_t k_range = round_up((k + splits - 1) / splits, 128);
     splits = (k + k_range - 1) / k_range;
     for (int z = 0; z < bt.count && splits > 1; ++z) {
-        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, nullptr, 0, di, st);
+        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
@@ -723,7 +714,7 @@ struct TcOps {
 template <int BN, int STAGES, int CG, int MC = 1>
 ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcmap, int32_t* c,
                          int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int c_mode, const DevInfo& di,
-                         cudaStream_t st, const int32_t* guard, const TcOps& ops) {
+                         cudaStream_t st, const TcOps& ops) {
     using S = tc::Smem<BN, STAGES, CG>;
     auto kern = tc_gemm_kernel<BN, STAGES, CG, MC>;
     static std::once_flag once[64];
@@ -762,18 +753,18 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         c_mode = 1;  // C already holds a partial sum: every split reduce-adds into it
     } else if (map.splits > 1) {
         c_mode = 1;
-        ngemm_status zs = zero_c(c, ldc, m, n, guard, 1, di, st);
+        ngemm_status zs = zero_c(c, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int grid = std::min(tiles * map.splits, units) * CG * MC;
     NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG * MC, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
-              static_cast<int>(n), num_kb, map, c_mode, guard);
+              static_cast<int>(n), num_kb, map, c_mode);
     return NGEMM_OK;
 }
 
 ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                             int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
-                            const int32_t* guard = nullptr, const TcOps& ops = TcOps()) {
+                            const TcOps& ops = TcOps()) {
     // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3): stage ragged
     // operands through a zero-padded scratch copy (padding K at the end is neutral).
     const uint8_t* a_use = a;
@@ -809,13 +800,13 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
     if (ops.accumulate && !c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "tcgen05: accumulating epilogue needs a TMA-describable C");
     if (s == NGEMM_OK) {
         switch (plan.cfg) {
-        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
-        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
-        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
-        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
-        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
-        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
-        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, guard, ops); break;
+        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         }
     }
     if (scratch) cudaFreeAsync(scratch, st);
@@ -828,28 +819,19 @@ cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int
     return cudaMemcpy2DAsync(dst, kp, src, k, k, rows, cudaMemcpyHostToDevice, st);
 }
 
-// HardwareSaturating for M > 16 without a host round trip (kernel_satfix.cuh):
+// HardwareSaturating on the tensor cores (kernel_satfix.cuh), no host round trip:
 //   1. sat_prep_a_kernel: max A -> guard[0], A in the fix kernel's pair-major tile layout
 //   2. sat_prep_b_kernel: B_safe = B with the pairs that could clamp zeroed, B's tiles, the
-//      dangerous-pair masks, per-tile counts, the total count and the hybrid threshold
-//                                                               -> guard[4..7]
-//   3. the dense CUDA-core kernel on (A, B)    runs when more than sat_hybrid_max_frac() of
-//      the pairs are dangerous (extreme inputs: the sparse fix would cost more) (selection 2)
-//   4. tcgen05 on (A, B_safe)                  runs when the selection is 0 or 1
-//   5. sat_fix_kernel adds the clamped sums of the dangerous pairs       (selection 1)
-// Every launch is enqueued; each reads the guard after griddepcontrol.wait and exits unless
-// selected, so the stream never synchronises with the host.
-// Used for M >= 256 and >= 2^29 MACs: below that the chain's fixed cost (five launches, ~25 us)
-// loses to the dense kernel even on the sparsest inputs (profiles/sweep_sat_hybrid_r1.log).
-// Above it, the break-even dangerous fraction (uniform vs sigma-32 B against the dense kernel)
-// grows with the work: ~0.04 at 0.5 G MACs, 0.36-0.47 at 1 G, 0.44-0.50 at 2 G, 0.54-0.59 at
-// 8-69 G.  NGEMM_SAT_HYBRID=1 forces the chain (tests), 0 disables it.
+//      per-row index lists of those pairs, per-tile-chunk counts, the total (guard[4..5])
+//   3. tcgen05 on (A, B_safe): the exact sums of every pair that cannot clamp
+//   4. sat_fix_kernel: adds the clamped sums of the listed pairs (exits at once if none)
+// Used for M >= 256 and >= 1e9 MACs (profiles/sweep_sat_hybrid_r1.log): below that the chain's
+// fixed cost (~20 us) loses to the dense CUDA-core kernel.  On uniform int8 B (~25 % of the
+// pairs listed) it is 1.2-2.1x faster than the dense kernel, on weight-like B (sigma 32,
+// ~0.4 %) 1.9-14x; rows whose pairs are all listed (config 4's extremes) take a list-free path.
+// NGEMM_SAT_HYBRID=1 forces the chain (tests), 0 disables it.
 constexpr int64_t kSatHybridMinM = 256;
-constexpr double kSatHybridMinWork = static_cast<double>(1ll << 29);
-double sat_hybrid_max_frac(int64_t m, int64_t n, int64_t k) {
-    const double w = static_cast<double>(m) * n * k;
-    return w < 1e9 ? 0.03 : w < 2e9 ? 0.35 : w < 8e9 ? 0.44 : 0.54;
-}
+constexpr double kSatHybridMinWork = 1e9;
 int sat_hybrid_env() {
     const char* e = std::getenv("NGEMM_SAT_HYBRID");
     return e ? std::atoi(e) : -1;
@@ -886,30 +868,27 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
         g_launches.fetch_add(1, std::memory_order_relaxed);
         return NGEMM_OK;
     };
+    // experiments only (timing probes): skip launches of the chain, results are then wrong
+    int skip = 0;
+    if (const char* e = std::getenv("NGEMM_SATFIX_SKIP")) skip = std::atoi(e);
     auto grid_for = [&](int64_t items) {
         return dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, di.sms * 16))));
     };
-    if (s == NGEMM_OK)
+    if (s == NGEMM_OK && !(skip & 1))
         s = launched(launch_k(sat_prep_a_kernel, grid_for(tm * chunks * 8 * (TM / 2)), dim3(256), 0, st, 1, 1, a, lda,
                               m, k, va, chunks, apm, guard));
-    if (s == NGEMM_OK) {
-        const unsigned long long thresh =
-            static_cast<unsigned long long>(sat_hybrid_max_frac(m, n, k) * static_cast<double>(n) *
-                                            static_cast<double>((k + 1) / 2));
+    if (s == NGEMM_OK && !(skip & 2))
         s = launched(launch_k(sat_prep_b_kernel, grid_for(tn * chunks * TN * 4), dim3(256), 0, st, 1, 1, b, ldb, n, k,
-                              vb, chunks, bsafe, lds, bt, lt, flags, guard, thresh));
-    }
-    // the dense kernel first: when not selected its CTAs exit at once, and when selected the
-    // tensor-core and fix grids behind it exit at once
-    if (s == NGEMM_OK) s = launch_simt(a, lda, b, ldb, c, ldc, m, n, k, NGEMM_SAT_HARDWARE, st, guard);
-    if (s == NGEMM_OK) s = launch_tcgen05(a, lda, reinterpret_cast<const int8_t*>(bsafe), lds, c, ldc, m, n, k, di, st, guard);
+                              vb, chunks, bsafe, lds, bt, lt, flags, guard));
+    if (s == NGEMM_OK && !(skip & 8))
+        s = launch_tcgen05(a, lda, reinterpret_cast<const int8_t*>(bsafe), lds, c, ldc, m, n, k, di, st);
     if (s == NGEMM_OK) {
         static std::once_flag once[64];
         int dev = 0;
         cudaGetDevice(&dev);
         std::call_once(once[dev & 63], [&] { s = set_smem(sat_fix_kernel, SMEM); });
     }
-    if (s == NGEMM_OK) {
+    if (s == NGEMM_OK && !(skip & 16)) {
         // one CTA per SM: ~3 waves of CTAs for balance (the TMA reduce-add epilogue makes K
         // splits cheap), >= 2 chunks per CTA when that still fills every SM so the two-stage
         // pipeline overlaps loads with math
@@ -1159,7 +1138,7 @@ ngemm_status launch_i16_tc(const int16_t* a, int64_t lda, const int16_t* b, int6
     const Term terms[4] = {{al, bl, {0, 0, 0, 0}}, {al, bh, {0, 1, 8, 1}}, {ah, bl, {1, 0, 8, 1}}, {ah, bh, {1, 1, 16, 1}}};
     for (const Term& t : terms) {
         if (s != NGEMM_OK) break;
-        s = launch_tcgen05(t.x, kp, reinterpret_cast<const int8_t*>(t.y), kp, c, ldc, m, n, kp, di, st, nullptr, t.ops);
+        s = launch_tcgen05(t.x, kp, reinterpret_cast<const int8_t*>(t.y), kp, c, ldc, m, n, kp, di, st, t.ops);
     }
     cudaFreeAsync(planes, st);
     return s;

@@ -228,28 +228,6 @@ __device__ __forceinline__ void tma_prefetch_tile_2d(const CUtensorMap* map, int
 // Let the dependent grid start launching (its CTAs run their prologue, then pdl_wait()).
 __device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
-// ---------------------------------------------------------------- saturation guard
-// The HardwareSaturating dispatcher's device-side decision, so the stream never synchronises
-// with the host (kernel_satfix.cuh).  guard (int32[16], zeroed by the host):
-//   [0]    = max a (u8)                             written by sat_prep_a_kernel
-//   [4..5] = u64 number of "dangerous" B pairs      written by sat_prep_b_kernel
-//   [6..7] = u64 threshold for the hybrid path      written by sat_prep_b_kernel
-// A pair (b0, b1) is dangerous when some a0, a1 in [0, max a] can push a0*b0 + a1*b1 out of
-// int16; every other pair's sum is exact, so those pairs can go to the tensor cores.
-// Selection: 0 = no dangerous pair (tensor cores alone), 1 = tensor cores on B with the
-// dangerous pairs zeroed + the CUDA-core fix of the dangerous pairs, 2 = dense CUDA-core kernel.
-__device__ __forceinline__ int sat_select(const int32_t* guard) {
-    const unsigned long long cnt = *reinterpret_cast<const volatile unsigned long long*>(guard + 4);
-    const unsigned long long thr = *reinterpret_cast<const volatile unsigned long long*>(guard + 6);
-    return cnt == 0 ? 0 : (cnt <= thr ? 1 : 2);
-}
-enum GuardRole { GUARD_SIMT = 0, GUARD_TC = 1, GUARD_FIX = 2 };
-// Whether the launch with this role runs under the guard's selection.
-__device__ __forceinline__ bool guard_runs(const int32_t* guard, int role) {
-    const int sel = sat_select(guard);
-    return role == GUARD_TC ? sel <= 1 : (role == GUARD_FIX ? sel == 1 : sel == 2);
-}
-
 // ---------------------------------------------------------------- cluster / DSMEM
 __device__ __forceinline__ uint32_t dsmem_ld_u32(uint32_t local_smem_addr, uint32_t cta) {
     uint32_t v;

@@ -366,12 +366,12 @@ def _normal_i8(rng, shape, sigma=32.0):
 @pytest.mark.parametrize("case", ["uniform", "normal", "extreme", "dense_frac", "sparse_edges", "safe_b"])
 def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
     """HardwareSaturating for M > 16 (kernel_satfix.cuh): tcgen05 on B with the pairs that could
-    clamp zeroed, plus the CUDA-core fix of those pairs — or the dense CUDA-core kernel when more
-    than 60 % of the pairs could clamp.  Every selection, ragged shapes (odd K, K < 256, K not a
-    multiple of 16, unaligned leading dimensions) must equal gemm_sat_oracle bit for bit."""
+    clamp zeroed, plus the CUDA-core fix of those pairs (list walk, or the list-free path for rows
+    whose pairs all could clamp).  Sparse, dense and empty lists, ragged shapes (odd K, K < 256, K
+    not a multiple of 16, unaligned leading dimensions) must equal gemm_sat_oracle bit for bit."""
     rng = np.random.default_rng(["uniform", "normal", "extreme", "dense_frac", "sparse_edges", "safe_b"].index(case))
-    # NGEMM_SAT_HYBRID=1 forces the chain below its size threshold (M >= 256, >= 2^29 MACs);
-    # 1000^3 and 512 x 1280 x 1024 take it by default
+    # NGEMM_SAT_HYBRID=1 forces the chain below its size threshold (M >= 256, >= 1e9 MACs);
+    # 1000^3 takes it by default
     monkeypatch.setenv("NGEMM_SAT_HYBRID", "1")
     shapes = [(300, 333, 777), (257, 390, 200), (40, 640, 1024), (129, 4100, 100), (1000, 1000, 1000),
               (512, 1280, 1024)]
@@ -385,7 +385,7 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
             a[:] = 255
             b = np.full((n, k), 127, np.int8)
             b[::3] = -128
-        elif case == "dense_frac":  # ~70 % of the pairs dangerous: the dense kernel runs
+        elif case == "dense_frac":  # ~70 % of the pairs can clamp: long lists, some full rows
             b = np.where(rng.random((n, k)) < 0.84, 127, rng.integers(-128, 128, (n, k))).astype(np.int8)
         elif case == "sparse_edges":  # a few dangerous pairs at chunk edges and in the odd-K tail
             b = rng.integers(-50, 51, (n, k), dtype=np.int8)
