@@ -274,7 +274,20 @@ __global__ void __launch_bounds__(satfix::THREADS, 1)
             };
             if (cnt == CHUNK / 2) {  // every pair of the row listed (extreme inputs): no list walk
 #pragma unroll 4
-                for (uint32_t j = 0; j < CHUNK / 2; j += 2) process(j, j + 1, true);
+                for (uint32_t j = 0; j < CHUNK / 2; j += 2) {
+                    const uint4 w1 = lds_v4(sa + (j << 9));
+                    const uint4 w2 = lds_v4(sa + ((j + 1) << 9));
+                    const uint32_t bw = lds_u32(sb + (j << 1));  // pairs j and j + 1 of B
+                    const uint32_t b1 = bw & 0xFFFFu, b2 = bw >> 16, b1h = bw << 16, b2h = bw & 0xFFFF0000u;
+                    const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+                    const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
+                        acc[nn][2 * q + 1] =
+                            sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
+                    }
+                }
             } else {
                 for (int e = 0; e < cnt; e += 4) {
                     const uint32_t idx = lds_u32(sl + e);  // four indices; entries past cnt are masked
@@ -308,7 +321,7 @@ __global__ void __launch_bounds__(satfix::THREADS, 1)
                               static_cast<int32_t>(u * TM + rb * 32));
         }
         tma_store_commit();
-        tma_store_wait<0>();
+        tma_store_wait_read<0>();  // smem must outlive the reads; the adds complete with the grid
     }
 }
 

@@ -889,12 +889,17 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
         std::call_once(once[dev & 63], [&] { s = set_smem(sat_fix_kernel, SMEM); });
     }
     if (s == NGEMM_OK && !(skip & 16)) {
-        // one CTA per SM: ~3 waves of CTAs for balance (the TMA reduce-add epilogue makes K
-        // splits cheap), >= 2 chunks per CTA when that still fills every SM so the two-stage
-        // pipeline overlaps loads with math
+        // One CTA per SM, so a launch runs in ceil(CTAs / SMs) waves; each CTA pays a fixed cost
+        // (chunk-list build, first load, epilogue reduce: ~one chunk's time) on top of its
+        // chunks.  Pick the K split minimising waves x (chunks per CTA + 1).
         const int64_t tiles = tn * tm;
-        int64_t splits = std::max<int64_t>(1, std::min<int64_t>(chunks, (3 * di.sms + tiles - 1) / tiles));
-        if (tiles * (chunks / 2) >= di.sms) splits = std::min<int64_t>(splits, std::max<int64_t>(1, chunks / 2));
+        int64_t splits = 1;
+        double best = 1e30;
+        for (int64_t sp = 1; sp <= std::min<int64_t>(chunks, 16); ++sp) {
+            const int64_t per_sp = (chunks + sp - 1) / sp;
+            const double t = static_cast<double>((tiles * sp + di.sms - 1) / di.sms) * static_cast<double>(per_sp + 1);
+            if (t < best - 1e-9) best = t, splits = sp;
+        }
         splits = std::max<int64_t>(splits, (chunks + MAX_LIST - 1) / MAX_LIST);  // the CTA's chunk list fits
         const int64_t per = (chunks + splits - 1) / splits;
         splits = (chunks + per - 1) / per;
