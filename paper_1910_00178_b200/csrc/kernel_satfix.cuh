@@ -17,10 +17,9 @@
 // Tiled operand layouts written by the two prep kernels (so the fix kernel streams whole
 // tiles with 1-D bulk copies into a double-buffered shared-memory pipeline):
 //   A_pm  [m-tile u][chunk c][pair j < 128][word p < 128]  u32 = (a[r0][2j], a[r0][2j+1],
-//          a[r1][2j], a[r1][2j+1]) with r0 = 8*(p/4)... see sat_prep_a_kernel: lane l of the fix
-//          kernel owns tile rows l + 32 t (t < 8); word p = 4l + q holds rows t = 2q and 2q + 1,
-//          so one LDS.128 gives a lane pair j of its 8 rows and one dp4a against (b0, b1, 0, 0)
-//          or (0, 0, b0, b1) is one row's pair sum
+//          a[r1][2j], a[r1][2j+1]) with p = 4 l + q, r0 = l + 64 q, r1 = r0 + 32: lane l of the
+//          fix kernel owns tile rows l + 32 t (t < 8), so one LDS.128 gives a lane pair j of its
+//          8 rows and one dp4a against (b0, b1, 0, 0) or (0, 0, b0, b1) is one row's pair sum
 //   B_t   [n-tile t][chunk c][row r < 128][256 bytes]   B's bytes, tile by tile
 //   L_t   [n-tile t][chunk c]{count[128] u8, list[128][128] u8}   per row, the indices of its
 //          dangerous pairs in the chunk (the fix walks these lists)

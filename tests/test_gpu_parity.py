@@ -403,10 +403,13 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
             assert (got == ref).all(), (case, "ld", int((got != ref).sum()))
 
 
-def test_host_entry_pipelined_pinned(cuda, oracle):
+@pytest.mark.parametrize("hybrid", ["0", "1"])
+def test_host_entry_pipelined_pinned(cuda, oracle, hybrid, monkeypatch):
     """ngemm_cuda_gemm_u8i8_host on PINNED host buffers takes the chunked H2D/compute/D2H
-    pipeline (C >= 64 MiB); result must equal the oracle in both modes."""
+    pipeline (C >= 64 MiB); result must equal the oracle in both modes.  hybrid=1 forces the
+    saturating tensor-core chain on every C tile (strided C sub-blocks, ragged tiles)."""
     import torch
+    monkeypatch.setenv("NGEMM_SAT_HYBRID", hybrid)
     L = _lib.load()
     # 4096^2 splits into 8 x 4 C tiles; 4000 x 4500 x 333 gives ragged row/column tiles and padded K
     for (m, n, k) in [(4096, 4096, 640), (4000, 4500, 333)]:
