@@ -22,5 +22,7 @@ want c2_mma_m1    && cap c2_mma_m1    "$E --shape 1x4096x1024" skinny_mma
 want c2_sat       && cap c2_sat       "$E --shape 16x4096x1024 --mode sat" skinny_sat
 want c2_tcskinny  && NGEMM_SKINNY_VARIANT=2 cap c2_tcskinny "$E --shape 16x4096x1024" tc_skinny
 want c2_rows_sat  && cap c2_rows_sat  "$E --shape 16x768x768 --mode sat" skinny_rows
-want c4_simt_sat  && cap c4_simt_sat  "$E --shape 2048x2048x2048 --mode sat" simt_gemm
+want c4_simt_sat  && cap c4_simt_sat  "$E --shape 2048x2048x2048 --mode sat --kernel simt" simt_gemm
+want c4_satfix_satu && cap c4_satfix_satu "$E --shape 2048x2048x2048 --mode sat --bdist uniform" sat_fix
+want c4_satfix_satn && cap c4_satfix_satn "$E --shape 2048x2048x2048 --mode sat --bdist normal" sat_fix
 want c3_tc        && cap c3_tc        "$E --shape 2048x4096x1024" tc_gemm
