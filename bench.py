@@ -195,6 +195,32 @@ def load_traffic(tag):
         return None
 
 
+# bench workload -> the committed ncu --set full summary of its dominant kernel (profiles/)
+NCU_TAGS = {"tcgen05:16384x16384x16384:exact": "c5_tc", "tcgen05:1024x1024x1024:exact": "c1_tc",
+            "tcgen05:2048x4096x1024:exact": "c3_tc", "skinny:16x4096x1024:exact": "c2_mma",
+            "skinny:1x4096x1024:exact": "c2_mma_m1", "skinny:16x4096x1024:sat": "c2_sat"}
+
+
+def load_ncu(tag):
+    """Tensor-pipe / clock figures of the dominant kernel from its committed ncu summary."""
+    name = NCU_TAGS.get(tag)
+    if not name:
+        return None
+    path = os.path.join(ROOT, "profiles", f"ncu_{name}.json")
+    try:
+        with open(path) as f:
+            cap = json.load(f)["full_capture"][0]
+    except Exception:
+        return None
+    pick = {"duration": "gpu__time_duration.sum", "sm_clock": "sm__cycles_elapsed.avg.per_second",
+            "tensor_pipe_active_pct": "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+            "tensor_mem_active_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+            "dram_read": "dram__bytes_read.sum", "dram_write": "dram__bytes_write.sum"}
+    out = {k: cap[v] for k, v in pick.items() if v in cap}
+    out["file"] = f"profiles/ncu_{name}.json"
+    return out
+
+
 def cpu_reference_sample(a_host, b_host, n, k, mode, target_s=12.0):
     """The reference's own CPU path on a bounded row sample of the workload: the unmodified
     reference compiled from its headers (oracle/_ref) when present, else our oracle port.
@@ -360,6 +386,7 @@ def run_ours(args):
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_gbs, "unit": "GB/s",
                 "frac": round(achieved / hbm_gbs, 4), "peak_basis": basis}
     roof["traffic"] = load_traffic(f"{picked}:{mr}x{N}x{K}:{args.mode}")
+    roof["ncu"] = load_ncu(f"{picked}:{mr}x{N}x{K}:{args.mode}")
     roof["algorithmic_bytes_per_launch"] = alg_bytes
     roof["algorithmic_ops_per_launch"] = alg_ops
     roof["kernel"] = picked

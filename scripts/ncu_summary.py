@@ -18,7 +18,8 @@ KEYS = ["gpu__time_duration.sum", "sm__cycles_elapsed.avg.per_second", "gpc__cyc
         "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
         "sm__pipe_shared_cycles_active.avg.pct_of_peak_sustained_active",
-        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active"]
+        "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum", "smsp__issue_active.avg.pct_of_peak_sustained_active",
+        "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active"]
 
 
 def raw(rep):
@@ -29,8 +30,9 @@ def raw(rep):
     for vals in rows[2:]:
         d = {"kernel": vals[hdr.index("Kernel Name")]}
         for k in KEYS:
-            if k in hdr:
-                i = hdr.index(k)
+            # some metrics carry a section prefix in the raw page (TPC.TriageCompute.<metric>)
+            i = hdr.index(k) if k in hdr else next((j for j, h in enumerate(hdr) if h.endswith("." + k)), None)
+            if i is not None:
                 d[k] = f"{vals[i]} {units[i]}".strip()
         res.append(d)
     return res
