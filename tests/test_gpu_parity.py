@@ -336,10 +336,14 @@ def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
             assert (dev_gemm(a, b, mode, "skinny", lda, ldb, ldc) == oracle.gemm(a, b, mode)).all(), (variant, m, n, k)
 
 
-def test_sat_mode_on_provably_safe_inputs(cuda, oracle):
+@pytest.mark.parametrize("hybrid", ["1", "-1"])
+def test_sat_mode_on_provably_safe_inputs(cuda, oracle, hybrid, monkeypatch):
     """HardwareSaturating on inputs that cannot saturate (the reference's safe range, u8 <= 127,
-    tuner.hpp:26-43): the device-side range proof routes the call to the tensor cores; the
-    result must still equal gemm_sat_oracle (== gemm_ref here).  Also the boundary cases."""
+    tuner.hpp:26-43): with max A measured on the device no pair is classified as clampable, so
+    the tensor cores compute everything and the fix kernel exits; the result must still equal
+    gemm_sat_oracle (== gemm_ref here).  Also the boundary cases around max A = 128 / 129.
+    hybrid=1 forces the tensor-core chain on every shape, -1 is the default dispatch."""
+    monkeypatch.setenv("NGEMM_SAT_HYBRID", hybrid)
     for (m, n, k) in ((512, 512, 1024), (1000, 700, 333), (2048, 2048, 2048)):
         a = oracle.mat_random_u8(m, k, 3, 0, 127)
         b = oracle.mat_random_i8(n, k, 4)
