@@ -44,7 +44,7 @@ def parse():
     p.add_argument("--config", default="c5")
     p.add_argument("--mode", choices=["exact", "sat"], default="exact")
     p.add_argument("--shape", default=None, help="override MxNxK (sweeps)")
-    p.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt", "skinny"])
+    p.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt", "skinny", "sat_hybrid"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--eager", action="store_true", help="never capture a CUDA graph")
@@ -271,7 +271,7 @@ def run_ours(args):
     name, M, N, K = workload(args)
     mode = EXACT if args.mode == "exact" else SAT
     kernel = {"auto": _lib.KERNEL_AUTO, "tcgen05": _lib.KERNEL_TCGEN05, "simt": _lib.KERNEL_SIMT,
-              "skinny": _lib.KERNEL_SKINNY}[args.kernel]
+              "skinny": _lib.KERNEL_SKINNY, "sat_hybrid": _lib.KERNEL_SAT_HYBRID}[args.kernel]
     from paper_1910_00178_b200 import dist as pdist
     r0, r1 = pdist.row_block(M, rank, world, 128)
     mr = r1 - r0

@@ -63,7 +63,10 @@ typedef enum {
     NGEMM_KERNEL_TCGEN05 = 1, /* tensor-core tcgen05.mma kind::i8 (exact mode only; AUTO runs the
                                  saturating mode on it too, for the pairs that cannot clamp) */
     NGEMM_KERNEL_SIMT = 2,    /* CUDA-core dp4a tiled kernel, both modes (the Engine::Emulated path) */
-    NGEMM_KERNEL_SKINNY = 3   /* memory-bound M <= 16 path, both modes */
+    NGEMM_KERNEL_SKINNY = 3,  /* memory-bound M <= 16 path, both modes */
+    NGEMM_KERNEL_SAT_HYBRID = 4 /* HardwareSaturating only, M > 16, C 16-byte aligned with ldc % 4 == 0:
+                                   tcgen05 on the pairs that cannot clamp + CUDA-core fix of the rest
+                                   (AUTO picks it for M >= 256 and >= 1e9 MACs) */
 } ngemm_kernel;
 
 /* PackedWeight metadata (layout.hpp:120-135; NGPT trailer layout.hpp:283-293).  h = 4 is the

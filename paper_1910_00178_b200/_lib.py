@@ -25,8 +25,9 @@ EXPORTS = [
 ]
 
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA, ERR_TUNE = range(9)
-KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT, KERNEL_SKINNY = range(4)
-KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_TCGEN05: "tcgen05", KERNEL_SIMT: "simt", KERNEL_SKINNY: "skinny"}
+KERNEL_AUTO, KERNEL_TCGEN05, KERNEL_SIMT, KERNEL_SKINNY, KERNEL_SAT_HYBRID = range(5)
+KERNEL_NAMES = {KERNEL_AUTO: "auto", KERNEL_TCGEN05: "tcgen05", KERNEL_SIMT: "simt", KERNEL_SKINNY: "skinny",
+                KERNEL_SAT_HYBRID: "sat_hybrid"}
 
 
 class PackedMeta(C.Structure):

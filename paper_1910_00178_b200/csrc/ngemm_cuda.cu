@@ -914,11 +914,11 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
 }
 
 int pick(int64_t m, int64_t n, int64_t k, int mode) {
-    (void)n;
-    (void)k;
     if (m <= kSkinnyMaxM) return NGEMM_KERNEL_SKINNY;
     if (mode == NGEMM_SAT_EXACT) return NGEMM_KERNEL_TCGEN05;
-    return NGEMM_KERNEL_SIMT;
+    const int env = sat_hybrid_env();
+    const bool big = m >= kSatHybridMinM && static_cast<double>(m) * n * k >= kSatHybridMinWork;
+    return (env == 1 || (env != 0 && big)) ? NGEMM_KERNEL_SAT_HYBRID : NGEMM_KERNEL_SIMT;
 }
 
 bool tuned_lookup(int64_t m, int64_t n, int64_t k, int mode, Choice* out);
@@ -936,21 +936,24 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
             kernel = ch.kernel;
         }
     }
-    const bool auto_kernel = kernel == NGEMM_KERNEL_AUTO;
     ngemm_status s = validate(a, lda, b, ldb, c, ldc, m, n, k, mode);
     if (s != NGEMM_OK) return s;
     int dev;
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    if (kernel == NGEMM_KERNEL_AUTO) kernel = pick(m, n, k, mode);
-    if (kernel == NGEMM_KERNEL_SIMT && mode == NGEMM_SAT_HARDWARE && auto_kernel && m > kSkinnyMaxM &&
-        reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0) {  // the fix adds into C by TMA reduce
-        const int env = sat_hybrid_env();
-        const bool big = m >= kSatHybridMinM && static_cast<double>(m) * n * k >= kSatHybridMinWork;
-        if (env == 1 || (env != 0 && big)) return launch_sat_hybrid(a, lda, b, ldb, c, ldc, m, n, k, di, st);
+    const bool c_tma = reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0;  // the fix adds into C by TMA
+    if (kernel == NGEMM_KERNEL_AUTO) {
+        kernel = pick(m, n, k, mode);
+        if (kernel == NGEMM_KERNEL_SAT_HYBRID && !c_tma) kernel = NGEMM_KERNEL_SIMT;
     }
     switch (kernel) {
+    case NGEMM_KERNEL_SAT_HYBRID:
+        if (mode != NGEMM_SAT_HARDWARE) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid is the HardwareSaturating path");
+        if (m <= kSkinnyMaxM) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid needs M > 16 (the skinny path covers M <= 16)");
+        if (!c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid needs a 16-byte aligned C with ldc % 4 == 0");
+        if (m > INT32_MAX - tc::BM || k > INT32_MAX - tc::BK) return fail(NGEMM_ERR_SHAPE, "sat_hybrid: dims too large");
+        return launch_sat_hybrid(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     case NGEMM_KERNEL_SIMT: return launch_simt(a, lda, b, ldb, c, ldc, m, n, k, mode, st);
     case NGEMM_KERNEL_SKINNY: return launch_skinny(a, lda, b, ldb, c, ldc, m, n, k, mode, di, st);
     case NGEMM_KERNEL_TCGEN05:
@@ -1694,8 +1697,8 @@ ngemm_status ngemm_cuda_tune(int64_t m, int64_t n, int64_t k, int sat_mode, int 
         c.kernel = NGEMM_KERNEL_SIMT;
         cands.push_back(c);
         if (sat_mode != NGEMM_SAT_EXACT && m > kSkinnyMaxM) {
-            Choice p;  // the hybrid dispatcher (tensor cores + sparse fix of the pairs that can clamp)
-            p.kernel = NGEMM_KERNEL_AUTO;
+            Choice p;  // tensor cores + sparse fix of the pairs that can clamp
+            p.kernel = NGEMM_KERNEL_SAT_HYBRID;
             cands.push_back(p);
         }
     }
@@ -1797,7 +1800,7 @@ ngemm_status load_store_file(const char* path, int* loaded) {
         ngemm_tune_record r{};
         if (!(is >> r.m >> r.n >> r.k >> r.sat_mode >> r.kernel >> r.tc_cfg >> r.tc_splits >> r.skinny_variant >>
               r.median_ns >> r.min_ns >> r.trials >> r.timestamp) ||
-            r.m < 1 || r.n < 1 || r.k < 1 || (r.sat_mode != 0 && r.sat_mode != 1) || r.kernel < 0 || r.kernel > 3)
+            r.m < 1 || r.n < 1 || r.k < 1 || (r.sat_mode != 0 && r.sat_mode != 1) || r.kernel < 0 || r.kernel > 4)
             return fail(NGEMM_ERR_CONFIG, "tune store: malformed record at line " + std::to_string(lineno));
         tuned_put(r);
         ++count;

@@ -40,7 +40,10 @@ def test_kernel_pick_policy():
     assert api.pick_kernel(1, 768, 768, api.SatMode.WIDENING_EXACT) == "skinny"
     assert api.pick_kernel(16, 4096, 1024, api.SatMode.HARDWARE_SATURATING) == "skinny"
     assert api.pick_kernel(1024, 1024, 1024, api.SatMode.WIDENING_EXACT) == "tcgen05"
-    assert api.pick_kernel(1024, 1024, 1024, api.SatMode.HARDWARE_SATURATING) == "simt"
+    # saturating: the tensor-core hybrid from M >= 256 and 1e9 MACs, the CUDA-core kernel below
+    assert api.pick_kernel(1024, 1024, 1024, api.SatMode.HARDWARE_SATURATING) == "sat_hybrid"
+    assert api.pick_kernel(512, 1024, 1024, api.SatMode.HARDWARE_SATURATING) == "simt"
+    assert api.pick_kernel(128, 4096, 4096, api.SatMode.HARDWARE_SATURATING) == "simt"
     assert api.pick_kernel(17, 64, 64, api.SatMode.WIDENING_EXACT) == "tcgen05"
 
 

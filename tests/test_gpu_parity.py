@@ -14,7 +14,7 @@ from paper_1910_00178_b200 import _lib, api
 pytestmark = pytest.mark.gpu
 
 KERNELS = {"simt": _lib.KERNEL_SIMT, "tcgen05": _lib.KERNEL_TCGEN05, "skinny": _lib.KERNEL_SKINNY,
-           "auto": _lib.KERNEL_AUTO}
+           "sat_hybrid": _lib.KERNEL_SAT_HYBRID, "auto": _lib.KERNEL_AUTO}
 
 
 def dev_gemm(a, b, mode, kernel="auto", lda=None, ldb=None, ldc=None):
@@ -403,8 +403,19 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
         got = dev_gemm(a, b, SAT, "auto")
         assert (got == ref).all(), (case, m, n, k, int((got != ref).sum()))
         if (m, n, k) == (300, 333, 777):  # ragged leading dimensions (no 16-byte vector loads)
-            got = dev_gemm(a, b, SAT, "auto", lda=k + 3, ldb=k + 5, ldc=n + 1)
+            got = dev_gemm(a, b, SAT, "auto", lda=k + 3, ldb=k + 5, ldc=n + 3)  # ldc % 4 == 0: TMA-able C
             assert (got == ref).all(), (case, "ld", int((got != ref).sum()))
+
+
+def test_sat_hybrid_explicit_kernel_id(cuda, oracle):
+    """NGEMM_KERNEL_SAT_HYBRID chosen explicitly: bit-exact on a small shape (below the AUTO size
+    rule); refused for exact mode, M <= 16 and a C that TMA cannot describe."""
+    a = oracle.mat_random_u8(100, 300, 5)
+    b = oracle.mat_random_i8(200, 300, 6)
+    assert (dev_gemm(a, b, SAT, "sat_hybrid") == oracle.gemm(a, b, SAT)).all()
+    for (aa, bb, mode, ldc) in ((a, b, EXACT, None), (a[:16], b, SAT, None), (a, b, SAT, 201)):
+        with pytest.raises(_lib.UnsupportedError):
+            dev_gemm(aa, bb, mode, "sat_hybrid", ldc=ldc)
 
 
 @pytest.mark.parametrize("hybrid", ["0", "1"])
