@@ -173,6 +173,14 @@ ngemm_status make_tmap_u8(CUtensorMap* map, const void* base, uint64_t inner, ui
     return NGEMM_OK;
 }
 
+// C through TMA (store / reduce-add epilogues): 16-byte aligned base and row pitch, and a row
+// length that is a whole number of 16-byte granules — a box straddling the last column writes
+// the whole trailing granule (measured: with N % 4 != 0 and ldc > N the bytes past column N-1
+// of each row change, scripts/probes/probe_ldc.py), so such C goes through direct stores.
+bool c_tma_ok(const int32_t* c, int64_t ldc, int64_t n) {
+    return reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0 && n % 4 == 0;
+}
+
 bool tma_ok(const void* p, int64_t ld) {
     return (reinterpret_cast<uintptr_t>(p) & 15) == 0 && ld % 16 == 0 && ld < (int64_t(1) << 39);
 }
@@ -788,7 +796,7 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
             ldb_use = kp;
         }
     }
-    const bool c_tma = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (ldc % 4 == 0);
+    const bool c_tma = c_tma_ok(c, ldc, n);
     const TcPlan plan = plan_tcgen05(m, n, k, di.sms, c_tma ? 1 : 0);
     const TcCfgInfo& ci = kTcCfg[plan.cfg];
     CUtensorMap ta, tb, tcm;
@@ -942,7 +950,7 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    const bool c_tma = reinterpret_cast<uintptr_t>(c) % 16 == 0 && ldc % 4 == 0;  // the fix adds into C by TMA
+    const bool c_tma = c_tma_ok(c, ldc, n);  // the sat fix adds into C by TMA reduce
     if (kernel == NGEMM_KERNEL_AUTO) {
         kernel = pick(m, n, k, mode);
         if (kernel == NGEMM_KERNEL_SAT_HYBRID && !c_tma) kernel = NGEMM_KERNEL_SIMT;
@@ -951,7 +959,7 @@ ngemm_status run_gemm(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ld
     case NGEMM_KERNEL_SAT_HYBRID:
         if (mode != NGEMM_SAT_HARDWARE) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid is the HardwareSaturating path");
         if (m <= kSkinnyMaxM) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid needs M > 16 (the skinny path covers M <= 16)");
-        if (!c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid needs a 16-byte aligned C with ldc % 4 == 0");
+        if (!c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "sat_hybrid needs a 16-byte aligned C with ldc % 4 == 0 and N % 4 == 0");
         if (m > INT32_MAX - tc::BM || k > INT32_MAX - tc::BK) return fail(NGEMM_ERR_SHAPE, "sat_hybrid: dims too large");
         return launch_sat_hybrid(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     case NGEMM_KERNEL_SIMT: return launch_simt(a, lda, b, ldb, c, ldc, m, n, k, mode, st);
@@ -1163,7 +1171,7 @@ ngemm_status run_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ld
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    const bool c_tma = (reinterpret_cast<uintptr_t>(c) % 16 == 0) && (ldc % 4 == 0);
+    const bool c_tma = c_tma_ok(c, ldc, n);
     bool tensor = c_tma && m > kSkinnyMaxM && static_cast<double>(m) * n * k >= kI16TensorMinWork &&
                   m <= INT32_MAX / 2 && k <= INT32_MAX / 4;
     if (const char* e = std::getenv("NGEMM_I16_PATH")) tensor = c_tma && std::strcmp(e, "tcgen05") == 0;  // tests

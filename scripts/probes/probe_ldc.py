@@ -1,0 +1,29 @@
+import os, sys
+sys.path.insert(0, "/root/repo"); sys.path.insert(0, ".")
+import numpy as np
+sys.path.insert(0, "tests")
+from test_gpu_parity import dev_gemm
+from oracle.oracle import Oracle, EXACT, SAT
+ora = Oracle()
+rng = np.random.default_rng(0)
+for (m, n, k) in [(300, 333, 777), (512, 640, 1024), (256, 200, 512)]:
+    a = rng.integers(0, 256, (m, k), dtype=np.uint8)
+    b = rng.integers(-128, 128, (n, k), dtype=np.int8)
+    for kern, mode, env in [("tcgen05", EXACT, "-1"), ("sat_hybrid", SAT, "-1"), ("simt", SAT, "-1")]:
+        for ldc in (n + 3, n + 7, n + 19):
+            if ldc % 4: continue
+            os.environ["NGEMM_SAT_HYBRID"] = env
+            try:
+                got = dev_gemm(a, b, mode, kern, ldc=ldc)
+                ok = (got == ora.gemm(a, b, mode)).all()
+                print(m, n, k, kern, ldc, "ok" if ok else "MISMATCH")
+            except AssertionError as e:
+                print(m, n, k, kern, ldc, "CANARY", e)
+    for skip in ("1", "2", "8", "16"):
+        os.environ["NGEMM_SATFIX_SKIP"] = skip
+        try:
+            dev_gemm(a, b, SAT, "sat_hybrid", ldc=n + 3)
+            print("skip", skip, "no canary hit")
+        except AssertionError as e:
+            print("skip", skip, "CANARY", str(e)[:60])
+    os.environ.pop("NGEMM_SATFIX_SKIP")

@@ -309,8 +309,11 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
     for splits, direct in (("1", "0"), ("1", "1"), ("2", "0"), ("3", "0")):
         monkeypatch.setenv("NGEMM_TC_SPLITS", splits)
         monkeypatch.setenv("NGEMM_TC_DIRECT", direct)  # TMA-store vs direct vector-store epilogue
+        # (300, 333, 777, 336): ldc % 4 == 0 but N % 4 != 0 — must not take the TMA epilogue (a box
+        # straddling the last column writes the whole trailing 16-byte granule, probe_ldc.py)
         for (m, n, k, ldc) in ((300, 520, 1100, None), (256, 256, 2048, 260), (129, 65, 640, None),
-                               (513, 300, 1024, 301), (600, 1024, 700, None), (256, 512, 128, 516)):
+                               (513, 300, 1024, 301), (600, 1024, 700, None), (256, 512, 128, 516),
+                               (300, 333, 777, 336)):
             a = oracle.mat_random_u8(m, k, m + cfg)
             b = oracle.mat_random_i8(n, k, n + cfg)
             got = dev_gemm(a, b, EXACT, "tcgen05", ldc=ldc)
@@ -377,8 +380,9 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
     # NGEMM_SAT_HYBRID=1 forces the chain below its size threshold (M >= 256, >= 1e9 MACs);
     # 1000^3 takes it by default
     monkeypatch.setenv("NGEMM_SAT_HYBRID", "1")
-    shapes = [(300, 333, 777), (257, 390, 200), (40, 640, 1024), (129, 4100, 100), (1000, 1000, 1000),
-              (512, 1280, 1024)]
+    # N % 4 != 0 (333) cannot take the TMA reduce-add: AUTO falls back to the CUDA-core kernel
+    shapes = [(300, 332, 777), (300, 333, 777), (257, 388, 200), (40, 640, 1024), (129, 4100, 100),
+              (1000, 1000, 1000), (512, 1280, 1024)]
     for (m, n, k) in shapes:
         a = rng.integers(0, 256, (m, k), dtype=np.uint8)
         if case == "uniform":
@@ -402,8 +406,8 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
         ref = oracle.gemm(a, b, SAT)
         got = dev_gemm(a, b, SAT, "auto")
         assert (got == ref).all(), (case, m, n, k, int((got != ref).sum()))
-        if (m, n, k) == (300, 333, 777):  # ragged leading dimensions (no 16-byte vector loads)
-            got = dev_gemm(a, b, SAT, "auto", lda=k + 3, ldb=k + 5, ldc=n + 3)  # ldc % 4 == 0: TMA-able C
+        if (m, n, k) in ((300, 332, 777), (300, 333, 777)):  # ragged leading dimensions (no 16-byte loads)
+            got = dev_gemm(a, b, SAT, "auto", lda=k + 3, ldb=k + 5, ldc=n + 4 - n % 4)  # ldc % 4 == 0
             assert (got == ref).all(), (case, "ld", int((got != ref).sum()))
 
 
@@ -413,7 +417,8 @@ def test_sat_hybrid_explicit_kernel_id(cuda, oracle):
     a = oracle.mat_random_u8(100, 300, 5)
     b = oracle.mat_random_i8(200, 300, 6)
     assert (dev_gemm(a, b, SAT, "sat_hybrid") == oracle.gemm(a, b, SAT)).all()
-    for (aa, bb, mode, ldc) in ((a, b, EXACT, None), (a[:16], b, SAT, None), (a, b, SAT, 201)):
+    for (aa, bb, mode, ldc) in ((a, b, EXACT, None), (a[:16], b, SAT, None), (a, b, SAT, 201),
+                                (a, b[:199], SAT, 200)):  # N % 4 != 0
         with pytest.raises(_lib.UnsupportedError):
             dev_gemm(aa, bb, mode, "sat_hybrid", ldc=ldc)
 
