@@ -55,6 +55,43 @@ __global__ void repack_kernel(PackedGeom g, const uint8_t* __restrict__ packed, 
     }
 }
 
+// Ragged operands -> TMA-describable copies (row pitch kp, a multiple of 16; bytes past k are
+// zero): rows of A then rows of B in one launch, one thread per 16-byte output chunk.  Source
+// rows with an unaligned pitch are read as aligned 4-byte words and realigned with funnel
+// shifts (5 loads per 16 output bytes instead of 16 byte loads).
+__global__ void stage_rows_kernel(const uint8_t* __restrict__ a, int64_t lda, int64_t ma,
+                                  const uint8_t* __restrict__ b, int64_t ldb, int64_t nb, int64_t k, int64_t kp,
+                                  uint8_t* __restrict__ da, uint8_t* __restrict__ db) {
+    pdl_launch_dependents();
+    pdl_wait();
+    const int64_t cpr = kp / 16, total = (ma + nb) * cpr;
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / cpr, c = i - r * cpr;
+        const bool is_a = r < ma;
+        const int64_t row = is_a ? r : r - ma;
+        const uint8_t* src = is_a ? a + row * lda : b + row * ldb;
+        uint8_t* dst = (is_a ? da : db) + row * kp + c * 16;
+        const int64_t k0 = c * 16;
+        const uintptr_t addr = reinterpret_cast<uintptr_t>(src + k0);
+        uint32_t w[4] = {0, 0, 0, 0};
+        if (k0 + 20 <= k && (k0 >= 4 || (addr & 3) == 0)) {  // the 20 bytes read stay inside the row
+            const uint32_t* p = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+            const uint32_t sh = static_cast<uint32_t>(addr & 3) * 8;
+            uint32_t x[5];
+#pragma unroll
+            for (int q = 0; q < 5; ++q) x[q] = __ldg(p + q);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) w[q] = __funnelshift_r(x[q], x[q + 1], sh);
+        } else {
+#pragma unroll
+            for (int t = 0; t < 16; ++t)
+                if (k0 + t < k) w[t >> 2] |= static_cast<uint32_t>(__ldg(src + k0 + t)) << (8 * (t & 3));
+        }
+        *reinterpret_cast<uint4*>(dst) = make_uint4(w[0], w[1], w[2], w[3]);
+    }
+}
+
 // Deterministic full-range operand fill for the tuner (splitmix64 of the element index).
 __global__ void fill_random_kernel(uint8_t* __restrict__ p, int64_t rows, int64_t cols, int64_t ld, uint64_t seed) {
     const int64_t total = rows * cols;

@@ -76,10 +76,10 @@ __global__ void sat_prep_a_kernel(const uint8_t* __restrict__ a, int64_t lda, in
         const int64_t u = tc / chunks, c = tc - u * chunks;
         // word rp = 4 l + q holds rows l + 64 q and l + 64 q + 32 of the tile
         const int64_t r0 = u * TM + (rp >> 2) + 64 * (rp & 3), r1 = r0 + 32, kb = c * CHUNK + s * 32;
-        const uint4 x0 = simt_load16(a, lda, r0, m, kb, k, vec_ok);
-        const uint4 x1 = simt_load16(a, lda, r0, m, kb + 16, k, vec_ok);
-        const uint4 y0 = simt_load16(a, lda, r1, m, kb, k, vec_ok);
-        const uint4 y1 = simt_load16(a, lda, r1, m, kb + 16, k, vec_ok);
+        const uint4 x0 = simt_load16<true>(a, lda, r0, m, kb, k, vec_ok);
+        const uint4 x1 = simt_load16<true>(a, lda, r0, m, kb + 16, k, vec_ok);
+        const uint4 y0 = simt_load16<true>(a, lda, r1, m, kb, k, vec_ok);
+        const uint4 y1 = simt_load16<true>(a, lda, r1, m, kb + 16, k, vec_ok);
         const uint32_t xa[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
         const uint32_t ya[8] = {y0.x, y0.y, y0.z, y0.w, y1.x, y1.y, y1.z, y1.w};
         uint32_t* dst = apm + tc * (A_TILE / 4) + (s * 16) * (TM / 2) + rp;
@@ -125,7 +125,7 @@ __global__ void sat_prep_b_kernel(const int8_t* __restrict__ b, int64_t ldb, int
         uint4 orig[4], safe[4];
 #pragma unroll
         for (int h = 0; h < 4; ++h) {
-            orig[h] = simt_load16(bu, ldb, row, n, c0 + 16 * h, k, vec_ok);
+            orig[h] = simt_load16<true>(bu, ldb, row, n, c0 + 16 * h, k, vec_ok);
             uint32_t w[4] = {orig[h].x, orig[h].y, orig[h].z, orig[h].w};
 #pragma unroll
             for (int e = 0; e < 4; ++e) {

@@ -28,12 +28,28 @@ constexpr int THREADS = 256;
 }  // namespace simt
 
 // Loads 16 bytes (4 K-words) of row `r` starting at byte `k0`; zero outside [0,rows)x[0,K).
+// WORDS: rows with an unaligned pitch are read as 5 aligned words realigned by funnel shifts
+// instead of 16 byte loads (the prep kernels; the tiled kernel keeps the lighter byte path,
+// which costs it no registers in its prefetch stage).
+template <bool WORDS = false>
 __device__ __forceinline__ uint4 simt_load16(const uint8_t* __restrict__ base, int64_t ld, int64_t r,
                                              int64_t rows, int64_t k0, int64_t K, bool vec_ok) {
     uint4 v = make_uint4(0, 0, 0, 0);
     if (r >= rows || k0 >= K) return v;
     const uint8_t* p = base + r * ld + k0;
     if (vec_ok && k0 + 16 <= K) return __ldg(reinterpret_cast<const uint4*>(p));
+    const uintptr_t addr = reinterpret_cast<uintptr_t>(p);
+    if (WORDS && k0 + 20 <= K && (k0 >= 4 || (addr & 3) == 0)) {
+        // unaligned row pitch: 5 aligned words, realigned by funnel shifts (the 20 bytes read
+        // stay inside the row)
+        const uint32_t* q = reinterpret_cast<const uint32_t*>(addr & ~uintptr_t(3));
+        const uint32_t sh = static_cast<uint32_t>(addr & 3) * 8;
+        uint32_t x[5];
+#pragma unroll
+        for (int i = 0; i < 5; ++i) x[i] = __ldg(q + i);
+        return make_uint4(__funnelshift_r(x[0], x[1], sh), __funnelshift_r(x[1], x[2], sh),
+                          __funnelshift_r(x[2], x[3], sh), __funnelshift_r(x[3], x[4], sh));
+    }
     uint32_t w[4] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < 16; ++i)

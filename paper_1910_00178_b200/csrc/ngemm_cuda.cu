@@ -363,26 +363,31 @@ ngemm_status launch_skinny_mode(const uint8_t* a, int64_t lda, const int8_t* b, 
     return launch_skinny_t<MODE, 16, 4>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
 }
 
-// Makes (a, lda) and (b, ldb) TMA-describable: ragged operands are copied into a zero-padded
-// scratch buffer with 16-byte row pitch (SURVEY.md §0 gotcha 3).  Caller frees *scratch.
+// Makes (a, lda) and (b, ldb) TMA-describable: ragged operands are copied by one
+// stage_rows_kernel launch into a zero-padded scratch buffer with 16-byte row pitch (SURVEY.md
+// §0 gotcha 3; padding K at the end is neutral).  Caller frees *scratch.
 ngemm_status stage_tma_operands(const uint8_t*& a, int64_t& lda, int64_t m, const uint8_t*& b, int64_t& ldb,
                                 int64_t n, int64_t k, uint8_t** scratch, cudaStream_t st) {
     *scratch = nullptr;
     const bool a_ok = tma_ok(a, lda), b_ok = tma_ok(b, ldb);
     if (a_ok && b_ok) return NGEMM_OK;
     const int64_t kp = round_up(k, 16);
-    const size_t bytes = static_cast<size_t>((a_ok ? 0 : m * kp) + (b_ok ? 0 : n * kp));
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(scratch), bytes, st));
-    uint8_t* p = *scratch;
+    const int64_t ma = a_ok ? 0 : m, nb = b_ok ? 0 : n;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(scratch), static_cast<size_t>((ma + nb) * kp), st));
+    uint8_t* da = *scratch;
+    uint8_t* db = *scratch + ma * kp;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>(((ma + nb) * (kp / 16) + 255) / 256,
+                                                                   dev_info(dev).sms * 8));
+    NG_LAUNCH(stage_rows_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, a, lda, ma, b, ldb, nb,
+              k, kp, da, db);
     if (!a_ok) {
-        NG_CUDA(cudaMemcpy2DAsync(p, kp, a, lda, k, m, cudaMemcpyDeviceToDevice, st));
-        a = p;
+        a = da;
         lda = kp;
-        p += m * kp;
     }
     if (!b_ok) {
-        NG_CUDA(cudaMemcpy2DAsync(p, kp, b, ldb, k, n, cudaMemcpyDeviceToDevice, st));
-        b = p;
+        b = db;
         ldb = kp;
     }
     return NGEMM_OK;
@@ -773,28 +778,14 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
 ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                             int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
                             const TcOps& ops = TcOps()) {
-    // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3): stage ragged
-    // operands through a zero-padded scratch copy (padding K at the end is neutral).
+    // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3)
     const uint8_t* a_use = a;
     const uint8_t* b_use = reinterpret_cast<const uint8_t*>(b);
     int64_t lda_use = lda, ldb_use = ldb;
     uint8_t* scratch = nullptr;
-    if (!tma_ok(a, lda) || !tma_ok(b, ldb)) {
-        const int64_t kp = round_up(k, 16);
-        const size_t bytes = static_cast<size_t>((tma_ok(a, lda) ? 0 : m * kp) + (tma_ok(b, ldb) ? 0 : n * kp));
-        NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&scratch), bytes, st));
-        uint8_t* p = scratch;
-        if (!tma_ok(a, lda)) {
-            NG_CUDA(cudaMemcpy2DAsync(p, kp, a, lda, k, m, cudaMemcpyDeviceToDevice, st));
-            a_use = p;
-            lda_use = kp;
-            p += m * kp;
-        }
-        if (!tma_ok(b, ldb)) {
-            NG_CUDA(cudaMemcpy2DAsync(p, kp, b, ldb, k, n, cudaMemcpyDeviceToDevice, st));
-            b_use = p;
-            ldb_use = kp;
-        }
+    {
+        ngemm_status ss = stage_tma_operands(a_use, lda_use, m, b_use, ldb_use, n, k, &scratch, st);
+        if (ss != NGEMM_OK) return ss;
     }
     const bool c_tma = c_tma_ok(c, ldc, n);
     const TcPlan plan = plan_tcgen05(m, n, k, di.sms, c_tma ? 1 : 0);
