@@ -504,11 +504,15 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
         }
     }
     if (const char* f = std::getenv("NGEMM_SKINNY_RG")) rg = std::atoi(f);  // experiments
+    // MT = 16 in a 1024-thread CTA is capped at 64 registers and spills: 16 warps at most
+    // (16 x 768 x 3072: 4.6 -> 3.85 us, profiles/sweep_skinny_warps_r1.log)
+    int64_t ks_use = MT >= 16 ? std::min<int64_t>(ks, 16) : ks;
+    if (const char* f = std::getenv("NGEMM_SKINNY_WARPS")) ks_use = std::atoi(f);  // experiments: 8 / 16 / 32
     if (rg == 2) return launch_skinny_mma_w<MT, 8, 2>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
     if (rg == 4) return launch_skinny_mma_w<MT, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
     if (rg == 8) return launch_skinny_mma_w<MT, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (ks <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (ks <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (ks_use <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (ks_use <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
     if (ks > 32 && splits == 1) splits = (ks + 31) / 32;
     return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
 }
