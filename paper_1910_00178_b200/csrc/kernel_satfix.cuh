@@ -21,8 +21,8 @@
 //          fix kernel owns tile rows l + 32 t (t < 8), so one LDS.128 gives a lane pair j of its
 //          8 rows and one dp4a against (b0, b1, 0, 0) or (0, 0, b0, b1) is one row's pair sum
 //   B_t   [n-tile t][chunk c][row r < 128][256 bytes]   B's bytes, tile by tile
-//   L_t   [n-tile t][chunk c]{count[128] u8, list[128][128] u8}   per row, the indices of its
-//          dangerous pairs in the chunk (the fix walks these lists)
+//   L_t   [n-tile t][chunk c]{count[128] u8, list[128][128] u8}   per row, its dangerous pairs
+//          in the chunk as B byte offsets 2j (the fix walks these lists)
 //   flags [n-tile t][chunk c]                           dangerous pairs in the tile chunk
 // Rows past M / N and bytes past K are zero.
 #pragma once
@@ -157,7 +157,10 @@ __global__ void sat_prep_b_kernel(const int8_t* __restrict__ b, int64_t ldb, int
         uint8_t* rec = lt + tc * L_TILE;
         if (q == 0) rec[r] = static_cast<uint8_t>(row_total);  // 0..128
         uint8_t* lst = rec + TN + r * (CHUNK / 2) + off;
-        for (uint32_t mb = mask, i = 0; mb; mb &= mb - 1, ++i) lst[i] = static_cast<uint8_t>(q * 32 + __ffs(mb) - 1);
+        // entries are B byte offsets 2j (<= 254): the fix kernel uses them unmasked — any byte,
+        // even a stale one past the count, addresses inside the row and inside the A tile
+        for (uint32_t mb = mask, i = 0; mb; mb &= mb - 1, ++i)
+            lst[i] = static_cast<uint8_t>(2 * (q * 32 + __ffs(mb) - 1));
         unsigned long long cnt = mine;
         for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
         if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&flags[tc], static_cast<uint32_t>(cnt));
@@ -251,17 +254,44 @@ __global__ void __launch_bounds__(satfix::THREADS, 1)
         const uint32_t st = smem_u32(smem) + (i & 1) * STAGE;
         const uint32_t sa = st + lane * 16;             // + j * 512: pair j of this lane's 8 rows
         const uint32_t sc = st + A_TILE + B_TILE;       // counts, then the index lists
+        // all 8 of this warp's rows fully listed (extreme inputs): pair-major loop, each pair of A
+        // words loaded once for the 8 rows instead of once per row
+        const uint32_t c_lo = lds_u32(sc + warp * NPW), c_hi = lds_u32(sc + warp * NPW + 4);
+        if (c_lo == 0x80808080u && c_hi == 0x80808080u) {
+            const uint32_t sb0 = st + A_TILE + warp * NPW * CHUNK;
+#pragma unroll 2
+            for (uint32_t j = 0; j < CHUNK / 2; j += 2) {
+                const uint4 w1 = lds_v4(sa + (j << 9));
+                const uint4 w2 = lds_v4(sa + ((j + 1) << 9));
+                const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+                const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+                for (int nn = 0; nn < NPW; ++nn) {
+                    const uint32_t bw = lds_u32(sb0 + nn * CHUNK + (j << 1));  // pairs j and j + 1
+                    const uint32_t b1 = bw & 0xFFFFu, b2 = bw >> 16, b1h = bw << 16, b2h = bw & 0xFFFF0000u;
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
+                        acc[nn][2 * q + 1] =
+                            sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
+                    }
+                }
+            }
+            __syncthreads();
+            continue;
+        }
 #pragma unroll
         for (int nn = 0; nn < NPW; ++nn) {
             const int nl = warp * NPW + nn;
             const uint32_t sb = st + A_TILE + nl * CHUNK;  // + j * 2: the row's pair j of B
             const uint32_t sl = sc + TN + nl * (CHUNK / 2);
             const int cnt = static_cast<int>(lds_u8(sc + nl));
-            auto process = [&](uint32_t j1, uint32_t j2, bool two) {
-                const uint4 w1 = lds_v4(sa + (j1 << 9));
-                const uint4 w2 = lds_v4(sa + (j2 << 9));
-                const uint32_t b1 = lds_u16(sb + (j1 << 1));
-                const uint32_t b2 = two ? lds_u16(sb + (j2 << 1)) : 0u;
+            // o1, o2: list entries = B byte offsets 2j; pair j of the lane's A rows sits at j * 512
+            auto process = [&](uint32_t o1, uint32_t o2, bool two) {
+                const uint4 w1 = lds_v4(sa + (o1 << 8));
+                const uint4 w2 = lds_v4(sa + (o2 << 8));
+                const uint32_t b1 = lds_u16(sb + o1);
+                const uint32_t b2 = two ? lds_u16(sb + o2) : 0u;
                 const uint32_t b1h = b1 << 16, b2h = b2 << 16;
                 const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
                 const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
@@ -288,10 +318,18 @@ __global__ void __launch_bounds__(satfix::THREADS, 1)
                     }
                 }
             } else {
-                for (int e = 0; e < cnt; e += 4) {
-                    const uint32_t idx = lds_u32(sl + e);  // four indices; entries past cnt are masked
-                    process(idx & 0x7Fu, (idx >> 8) & 0x7Fu, e + 1 < cnt);
-                    if (e + 2 < cnt) process((idx >> 16) & 0x7Fu, (idx >> 24) & 0x7Fu, e + 3 < cnt);
+                // whole groups of four entries, then a tail of up to three (no per-pair guards)
+                const int full = cnt & ~3;
+                for (int e = 0; e < full; e += 4) {
+                    const uint32_t idx = lds_u32(sl + e);
+                    process(__byte_perm(idx, 0, 0x4440), __byte_perm(idx, 0, 0x4441), true);
+                    process(__byte_perm(idx, 0, 0x4442), __byte_perm(idx, 0, 0x4443), true);
+                }
+                const int tail = cnt - full;
+                if (tail != 0) {
+                    const uint32_t idx = lds_u32(sl + full);
+                    process(__byte_perm(idx, 0, 0x4440), __byte_perm(idx, 0, 0x4441), tail >= 2);
+                    if (tail == 3) process(__byte_perm(idx, 0, 0x4442), __byte_perm(idx, 0, 0x4442), false);
                 }
             }
         }
