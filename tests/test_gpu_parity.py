@@ -381,8 +381,9 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
     # 1000^3 takes it by default
     monkeypatch.setenv("NGEMM_SAT_HYBRID", "1")
     # N % 4 != 0 (333) cannot take the TMA reduce-add: AUTO falls back to the CUDA-core kernel
+    # (260, 256, 40000): 157 K chunks > the fix kernel's 128-chunk list, so K is split on the host
     shapes = [(300, 332, 777), (300, 333, 777), (257, 388, 200), (40, 640, 1024), (129, 4100, 100),
-              (1000, 1000, 1000), (512, 1280, 1024)]
+              (1000, 1000, 1000), (512, 1280, 1024), (260, 256, 40000)]
     for (m, n, k) in shapes:
         a = rng.integers(0, 256, (m, k), dtype=np.uint8)
         if case == "uniform":
