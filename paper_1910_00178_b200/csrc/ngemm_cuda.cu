@@ -830,8 +830,9 @@ cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int
 //   4. sat_fix_kernel: adds the clamped sums of the listed pairs (exits at once if none)
 // Used for M >= 256 and >= 1e9 MACs (profiles/sweep_sat_hybrid_r1.log): below that the chain's
 // fixed cost (~20 us) loses to the dense CUDA-core kernel.  On uniform int8 B (~25 % of the
-// pairs listed) it is 1.2-2.1x faster than the dense kernel, on weight-like B (sigma 32,
-// ~0.4 %) 1.9-14x; rows whose pairs are all listed (config 4's extremes) take a list-free path.
+// pairs listed) it is 1.5-2.9x faster than the dense kernel, on weight-like B (sigma 32,
+// ~0.4 %) 2.2-14x; rows whose pairs are all listed (config 4's extremes) take a list-free path
+// (1.2x slower than the dense kernel there).
 // NGEMM_SAT_HYBRID=1 forces the chain (tests), 0 disables it.
 constexpr int64_t kSatHybridMinM = 256;
 constexpr double kSatHybridMinWork = 1e9;
