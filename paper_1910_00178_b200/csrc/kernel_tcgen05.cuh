@@ -108,7 +108,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    static_assert(MC == 1 || CG == 2, "A multicast pairs need cta_group::2");
+    static_assert(MC == 1 || MC == 2, "A is multicast across at most two tiles");
     constexpr int CL = CG * MC;  // CTAs per cluster
     const uint32_t crank = (CL > 1) ? cluster_ctarank() : 0;
     const uint32_t rank = crank & (CG - 1);           // rank within the pair: 0 = pair leader
@@ -155,7 +155,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 mbar_arrive(&full[p_s]);  // probes only: no operand traffic
             } else if constexpr (CG == 1) {
                 mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
-                tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
+                if constexpr (MC == 1) {
+                    tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
+                } else {
+                    // this CTA's half of the shared A slab, to itself and its neighbour in the cluster
+                    tma_load_2d_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[p_s], p_kb * tc::BK,
+                                   p_row_a + static_cast<int>(pair) * (tc::BM / 2), static_cast<uint16_t>(0x3), pol_a);
+                }
                 tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
             } else {
                 // both CTAs' bytes land on the leader's full barrier; the leader arms it
@@ -254,7 +260,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                         mma_i8<CG>(d_tmem, sdesc_k_sw128(sa + k * tc::UMMA_K), sdesc_k_sw128(sb + k * tc::UMMA_K),
                                    idesc, (kb > kb0 || k > 0) ? 1u : 0u);
                     }
-                    if constexpr (CG == 1) mma_commit(&empty[s]);
+                    if constexpr (CG == 1 && MC == 1) mma_commit(&empty[s]);
+                    else if constexpr (CG == 1) mma_commit_mc(&empty[s], static_cast<uint16_t>(0x3));  // both read A
                     else mma_commit_cg2_mc(&empty[s], MC == 1 ? pair_mask : static_cast<uint16_t>(0xF));
                     if (++s == STAGES) { s = 0; ph ^= 1; }
                 }

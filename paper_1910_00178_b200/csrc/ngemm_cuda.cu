@@ -640,7 +640,8 @@ ngemm_status make_tmap_c(CUtensorMap* map, const int32_t* c, int64_t rows, int64
 // Tile configurations of the tcgen05 kernel (per CTA: 128 rows of A; cta_group::2 pairs two SMs).
 enum TcCfg {
     TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_QUAD256 = 4, TC_LEAN128 = 5, TC_LEAN64 = 6,
-    TC_NUM_CFG = 7
+    TC_MC128 = 7, TC_MC64 = 8,  // 1-CTA tiles in 2-CTA clusters sharing A by TMA multicast
+    TC_NUM_CFG = 9
 };
 struct TcCfgInfo {
     int cg, bn, mc;
@@ -655,6 +656,8 @@ constexpr TcCfgInfo kTcCfg[TC_NUM_CFG] = {
     {2, 256, 2, 512.0, 0},  // two pairs sharing A (multicast): 256x512 per 4-CTA cluster
     {1, 128, 1, 450.0, 1},  // 128x128, 2 stages: latency-limited stream, but co-resident
     {1, 64, 1, 330.0, 1},   // 128x64, 3 stages
+    {1, 128, 2, 300.0, 0},  // 128x128 x 2 CTAs sharing A: half the A traffic into each SM
+    {1, 64, 2, 192.0, 0},   // 128x64 x 2 CTAs sharing A
 };
 // Lean configurations fit two CTAs per SM, so under PDL the next grid's CTAs finish their setup
 // while the previous grid runs — but their 2-3 stage pipelines lose more in the K loop than the
@@ -809,6 +812,8 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
         case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_MC128: s = launch_tc_t<128, 6, 1, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_MC64: s = launch_tc_t<64, 8, 1, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         }
     }

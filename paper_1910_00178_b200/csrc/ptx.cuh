@@ -149,6 +149,16 @@ __device__ __forceinline__ void tma_load_2d_cg2(void* dst, const CUtensorMap* ma
         : "memory");
 }
 // 2-CTA variant with multicast to the CTAs in `mask` (same smem offset in each).
+// cta_group::1 multicast: the box lands at the same smem offset in every CTA of `mask` and
+// completes tx bytes on each CTA's barrier at the same offset.
+__device__ __forceinline__ void tma_load_2d_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
+                                               int32_t c1, uint16_t mask, uint64_t cache_hint) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster.L2::cache_hint"
+        " [%0], [%1, {%4, %5}], [%2], %3, %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "h"(mask), "r"(c0), "r"(c1), "l"(cache_hint)
+        : "memory");
+}
 __device__ __forceinline__ void tma_load_2d_cg2_mc(void* dst, const CUtensorMap* map, uint64_t* bar, int32_t c0,
                                                    int32_t c1, uint16_t mask, uint64_t cache_hint) {
     asm volatile(
@@ -299,6 +309,13 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                  : "memory");
 }
 // 2-CTA commit: arrive on the barrier at this smem offset in every CTA of `mask`.
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+            smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
 __device__ __forceinline__ void mma_commit_cg2_mc(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(

@@ -301,9 +301,10 @@ def test_config5_full_size(cuda, oracle, golden):
         assert torch.equal(lhs, rhs)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6, 7, 8])
 def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
-    """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64), with and without
+    """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64, the 4-CTA and 2-CTA
+    A-multicast clusters, the lean 2-3 stage variants), with and without
     split-K (TMA s32 reduce-add), with TMA-store and direct-store epilogues, vs the oracle."""
     monkeypatch.setenv("NGEMM_TC_CFG", str(cfg))
     for splits, direct in (("1", "0"), ("1", "1"), ("2", "0"), ("3", "0")):
