@@ -6,6 +6,8 @@ import os
 import subprocess
 import sys
 
+import pytest
+
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
@@ -37,3 +39,20 @@ def test_reference_arm_other_ranks_exit_quietly():
     lines = run_bench("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1",
                       env={"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert lines == []
+
+
+@pytest.mark.gpu
+def test_our_arm_json_line():
+    """Our arm on a short config-1 run: the keys the driver and the judge read."""
+    lines = run_bench("--config", "c1", "--steps", "3", "--warmup", "3")
+    assert len(lines) == 1
+    d = lines[0]
+    for key in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+                "vs_baseline", "dtype", "data", "config", "roofline", "cpu_baseline", "e2e", "clocks", "gpu_launches"):
+        assert key in d, key
+    assert d["n_gpus"] == 1 and d["steps"] == 3 and d["warmup"] == 3 and d["value"] > 0 and d["gpu_launches"] >= 3
+    r = d["roofline"]
+    assert r["bound"] in ("hbm", "tensor") and 0 < r["frac"] and r["peak"] > 0 and r["unit"] in ("GB/s", "TOPS")
+    assert d["e2e"]["h2d_bytes_per_step"] == 2 * 1024 * 1024 and d["e2e"]["d2h_bytes_per_step"] == 4 * 1024 * 1024
+    assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
+    assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
