@@ -22,6 +22,7 @@ EXPORTS = [
     "ngemm_cuda_launch_count", "ngemm_cuda_gemm_i16", "ngemm_cuda_gemm_i16_host", "ngemm_cuda_gemm_packed_i16",
     "ngemm_cuda_gemm_packed_resident_host", "ngemm_cuda_device", "ngemm_cuda_tune", "ngemm_cuda_tune_store_save",
     "ngemm_cuda_tune_store_load", "ngemm_cuda_tune_clear", "ngemm_cuda_gemm_u8i8_strided_batched",
+    "ngemm_cuda_gemm_u8i8_requant",
 ]
 
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA, ERR_TUNE = range(9)
@@ -63,6 +64,7 @@ def load():
         L.ngemm_cuda_gemm_u8i8_ex.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, i32, i32, vp]
         L.ngemm_cuda_gemm_u8i8_strided_batched.argtypes = [vp, i64, i64, vp, i64, i64, vp, i64, i64, i64, i64, i64,
                                                             i64, i32, vp]
+        L.ngemm_cuda_gemm_u8i8_requant.argtypes = [vp, i64, vp, i64, vp, i64, i64, i64, i64, vp, vp, i32, i32, vp]
         L.ngemm_cuda_repack.argtypes = [C.POINTER(PackedMeta), vp, vp, i64, vp]
         L.ngemm_cuda_packed_validate.argtypes = [C.POINTER(PackedMeta)]
         L.ngemm_cuda_packed_upload.argtypes = [C.POINTER(PackedMeta), vp, C.c_size_t, C.POINTER(vp)]

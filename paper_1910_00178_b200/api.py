@@ -257,6 +257,30 @@ def gemm_device(a, b, c=None, mode: SatMode = SatMode.WIDENING_EXACT, kernel: in
     return c
 
 
+def gemm_device_requant(a, b, scale, bias=None, zero_point: int = 0, out=None,
+                        mode: SatMode = SatMode.WIDENING_EXACT, stream=None):
+    """int8 out[M, N] = clamp(rint(float(A.B^T + bias) * scale) + zero_point) on CUDA tensors, the
+    requantisation fused into the tcgen05 epilogue for exact mode and M > 16
+    (ngemm_cuda_gemm_u8i8_requant).  scale: float32 [N], bias: int32 [N] or None."""
+    import torch
+    if a.dtype != torch.uint8 or b.dtype != torch.int8:
+        raise UnsupportedError(f"gemm: no kernel path for {a.dtype} x {b.dtype}")
+    if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
+        raise ShapeError(f"gemm: K mismatch, A is {tuple(a.shape)} but B is {tuple(b.shape)}")
+    m, k = a.shape
+    n = b.shape[0]
+    if scale.dtype != torch.float32 or scale.shape != (n,) or (bias is not None and
+                                                             (bias.dtype != torch.int32 or bias.shape != (n,))):
+        raise ShapeError("requant: scale must be float32 [N] and bias int32 [N]")
+    if out is None:
+        out = torch.empty((m, n), dtype=torch.int8, device=a.device)
+    check(_lib.load().ngemm_cuda_gemm_u8i8_requant(
+        a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0), m, n, k,
+        scale.data_ptr(), bias.data_ptr() if bias is not None else None, int(zero_point), int(mode),
+        _stream_ptr(stream)))
+    return out
+
+
 def gemm_device_batched(a, b, c=None, mode: SatMode = SatMode.WIDENING_EXACT, stream=None):
     """C[z] = A[z] * B[z]^T for a batch of GEMMs of one shape, on CUDA torch tensors.
 

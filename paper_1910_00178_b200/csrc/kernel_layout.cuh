@@ -92,6 +92,22 @@ __global__ void stage_rows_kernel(const uint8_t* __restrict__ a, int64_t lda, in
     }
 }
 
+// Requantisation of an int32 C to int8 (the unfused form of the tcgen05 kernel's c_mode 4, same
+// arithmetic): out[r][c] = clamp(rint(float(C[r][c] + bias[c]) * scale[c]) + zp, -128, 127).
+__global__ void requant_kernel(const int32_t* __restrict__ c, int64_t ldc, int64_t m, int64_t n,
+                               const float* __restrict__ scale, const int32_t* __restrict__ bias, int zp,
+                               int8_t* __restrict__ out, int64_t ldo) {
+    pdl_launch_dependents();
+    pdl_wait();
+    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m * n;
+         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t r = i / n, col = i - r * n;
+        const uint32_t acc = static_cast<uint32_t>(c[r * ldc + col]) + static_cast<uint32_t>(bias ? bias[col] : 0);
+        const float prod = fminf(fmaxf(__fmul_rn(__int2float_rn(static_cast<int32_t>(acc)), scale[col]), -1.0e6f), 1.0e6f);
+        out[r * ldo + col] = static_cast<int8_t>(max(-128, min(127, __float2int_rn(prod) + zp)));
+    }
+}
+
 // Deterministic full-range operand fill for the tuner (splitmix64 of the element index).
 __global__ void fill_random_kernel(uint8_t* __restrict__ p, int64_t rows, int64_t cols, int64_t ld, uint64_t seed) {
     const int64_t total = rows * cols;

@@ -70,6 +70,12 @@ struct TileMap {
     int trace_id;                  // trace build: launch index for the phase stamps (-1 otherwise)
     int a_signed, b_signed;        // operand formats (u8 x s8 for the NGEMM path; any mix for i16 planes)
     int shift;                     // epilogue: C (+)= acc << shift  (i16 byte-plane decomposition)
+    // c_mode 4, fused requantisation: out[r][c] = clamp(rint(float(acc + bias[c]) * scale[c]) + zp)
+    const float* rq_scale;
+    const int32_t* rq_bias;        // may be null
+    int8_t* rq_out;
+    int64_t rq_ldo;
+    int rq_zp;
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -95,7 +101,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                    int num_kb_total, TileMap map, int c_mode) {
     // c_mode: 0 = TMA tensor store of C (SWIZZLE_128B staging), 1 = TMA reduce-add into a
     // zeroed C (split-K), 2 = direct scalar stores (C not TMA-describable), 3 = direct 16-byte
-    // vector stores (aligned C, single-wave grids).
+    // vector stores (aligned C, single-wave grids), 4 = fused requantisation to int8 (map.rq_*).
     TC_TRACE_KEEP(0);
     using S = tc::Smem<BN, STAGES, CG>;
     constexpr int UMMA_M = tc::BM * CG;
@@ -301,6 +307,37 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     for (int j = 0; j < 32; ++j) v[j] <<= map.shift;  // mod 2^32, like the accumulator
                 }
                 const int col0 = tn * BN + c;
+                if (c_mode == 4) {
+                    // fused requantisation to int8: each lane loads one column's scale / bias and
+                    // the warp broadcasts them; lane = row, 32 int8 per row, two 16-byte stores
+                    const int col = col0 + lane;
+                    const float my_s = col < N ? __ldg(map.rq_scale + col) : 0.0f;
+                    const int32_t my_b = (map.rq_bias != nullptr && col < N) ? __ldg(map.rq_bias + col) : 0;
+                    uint32_t packed[8];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const float sj = __shfl_sync(0xffffffffu, my_s, j);
+                        const int32_t bj = __shfl_sync(0xffffffffu, my_b, j);
+                        const float y = __int2float_rn(static_cast<int32_t>(v[j] + static_cast<uint32_t>(bj)));
+                        const float prod = fminf(fmaxf(__fmul_rn(y, sj), -1.0e6f), 1.0e6f);
+                        const int q = max(-128, min(127, __float2int_rn(prod) + map.rq_zp));
+                        if ((j & 3) == 0) packed[j >> 2] = 0;
+                        packed[j >> 2] |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * (j & 3));
+                    }
+                    const int64_t row = static_cast<int64_t>(row0) + lane;
+                    if (row < M) {
+                        int8_t* orow = map.rq_out + row * map.rq_ldo + col0;
+                        if (col0 + 32 <= N && (reinterpret_cast<uintptr_t>(orow) & 15) == 0) {
+                            st_global_v4(orow, packed[0], packed[1], packed[2], packed[3]);
+                            st_global_v4(orow + 16, packed[4], packed[5], packed[6], packed[7]);
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 32; ++j)
+                                if (col0 + j < N) orow[j] = static_cast<int8_t>((packed[j >> 2] >> (8 * (j & 3))) & 0xFFu);
+                        }
+                    }
+                    continue;
+                }
                 if (c_mode <= 1) {
                     uint8_t* buf = stage_c + cbuf * S::STAGE_C_BYTES;
                     // the TMA store that last read this buffer must be done with it

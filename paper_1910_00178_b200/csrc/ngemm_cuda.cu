@@ -729,6 +729,12 @@ struct TcOps {
     int a_signed = 0, b_signed = 1;
     int shift = 0;       // C (+)= acc << shift
     int accumulate = 0;  // 1: TMA reduce-add into C (C holds the previous planes' sum)
+    // fused requantisation (c_mode 4): int8 out instead of C
+    const float* rq_scale = nullptr;
+    const int32_t* rq_bias = nullptr;
+    int8_t* rq_out = nullptr;
+    int64_t rq_ldo = 0;
+    int rq_zp = 0;
 };
 
 template <int BN, int STAGES, int CG, int MC = 1>
@@ -763,6 +769,15 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.a_signed = ops.a_signed;
     map.b_signed = ops.b_signed;
     map.shift = ops.shift;
+    map.rq_scale = ops.rq_scale;
+    map.rq_bias = ops.rq_bias;
+    map.rq_out = ops.rq_out;
+    map.rq_ldo = ops.rq_ldo;
+    map.rq_zp = ops.rq_zp;
+    if (ops.rq_out != nullptr) {
+        c_mode = 4;  // the requantised value needs the whole K sum: no split
+        map.splits = 1;
+    }
 #ifdef NGEMM_TRACE
     if (const char* e = std::getenv("NGEMM_TC_DBG")) map.dbg = std::atoi(e);  // trace build only
     map.trace_id = g_trace_next++;
@@ -794,7 +809,8 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
         ngemm_status ss = stage_tma_operands(a_use, lda_use, m, b_use, ldb_use, n, k, &scratch, st);
         if (ss != NGEMM_OK) return ss;
     }
-    const bool c_tma = c_tma_ok(c, ldc, n);
+    const bool rq = ops.rq_out != nullptr;  // fused requantisation: no C, no split-K
+    const bool c_tma = !rq && c_tma_ok(c, ldc, n);
     const TcPlan plan = plan_tcgen05(m, n, k, di.sms, c_tma ? 1 : 0);
     const TcCfgInfo& ci = kTcCfg[plan.cfg];
     CUtensorMap ta, tb, tcm;
@@ -1362,6 +1378,41 @@ ngemm_status ngemm_cuda_gemm_u8i8_ex(const uint8_t* a, int64_t lda, const int8_t
                                      int64_t ldc, int64_t m, int64_t n, int64_t k, int sat_mode, int kernel,
                                      void* stream) {
     return run_gemm(a, lda, b, ldb, c, ldc, m, n, k, sat_mode, kernel, static_cast<cudaStream_t>(stream));
+}
+
+ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int8_t* out,
+                                          int64_t ldo, int64_t m, int64_t n, int64_t k, const float* scale,
+                                          const int32_t* bias, int zero_point, int sat_mode, void* stream) {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    ngemm_status s = validate(a, lda, b, ldb, out, ldo, m, n, k, sat_mode);
+    if (s != NGEMM_OK) return s;
+    if (!scale) return fail(NGEMM_ERR_SHAPE, "requant: null scale");
+    int dev;
+    DevInfo di;
+    s = current_device(&dev, &di);
+    if (s != NGEMM_OK) return s;
+    if (sat_mode == NGEMM_SAT_EXACT && m > kSkinnyMaxM && m <= INT32_MAX - tc::BM && k <= INT32_MAX - tc::BK) {
+        TcOps ops;
+        ops.rq_scale = scale;
+        ops.rq_bias = bias;
+        ops.rq_out = out;
+        ops.rq_ldo = ldo;
+        ops.rq_zp = zero_point;
+        return launch_tcgen05(a, lda, b, ldb, nullptr, n, m, n, k, di, st, ops);
+    }
+    // other shapes / the saturating mode: C in scratch, then the same arithmetic unfused
+    int32_t* cbuf = nullptr;
+    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cbuf), static_cast<size_t>(m * n) * 4, st));
+    s = run_gemm(a, lda, b, ldb, cbuf, n, m, n, k, sat_mode, NGEMM_KERNEL_AUTO, st);
+    if (s == NGEMM_OK) {
+        const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((m * n + 255) / 256, di.sms * 8));
+        cudaError_t e = launch_k(requant_kernel, dim3(static_cast<unsigned>(blocks)), dim3(256), 0, st, 1, 1, cbuf, n,
+                                 m, n, scale, bias, zero_point, out, ldo);
+        if (e != cudaSuccess) s = fail(NGEMM_ERR_CUDA, std::string("launch: ") + cudaGetErrorString(e));
+        else g_launches.fetch_add(1, std::memory_order_relaxed);
+    }
+    cudaFreeAsync(cbuf, st);
+    return s;
 }
 
 ngemm_status ngemm_cuda_packed_validate(const ngemm_packed_meta* meta) { return validate_meta(meta); }

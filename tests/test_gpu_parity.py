@@ -545,3 +545,43 @@ def test_i16_paths_vs_reference_golden(cuda, oracle, golden, path, monkeypatch):
         a = rng.integers(-32768, 32768, size=(m, k), dtype=np.int16)
         b = rng.integers(-32768, 32768, size=(n, k), dtype=np.int16)
         assert (_dev_gemm_i16(a, b) == oracle.gemm_i16(a, b)).all(), (path, m, n, k)
+
+
+def requant_ref(c, scale, bias, zp):
+    """The fused requantisation's arithmetic in numpy (ngemm_cuda.h): int32 + bias wraps,
+    float32 round-to-nearest conversion, one fp32 multiply, rint (half to even), clamp."""
+    acc = c.astype(np.int64) + (bias.astype(np.int64) if bias is not None else 0)
+    acc = ((acc + 2**31) % 2**32 - 2**31).astype(np.int32)
+    prod = np.clip(acc.astype(np.float32) * scale.astype(np.float32), np.float32(-1e6), np.float32(1e6))
+    return np.clip(np.rint(prod).astype(np.int64) + zp, -128, 127).astype(np.int8)
+
+
+@pytest.mark.parametrize("mode", [EXACT, SAT])
+def test_fused_requant_epilogue(cuda, oracle, mode):
+    """ngemm_cuda_gemm_u8i8_requant: exact mode, M > 16 requantises in the tcgen05 epilogue (int32
+    C never stored); M <= 16 and the saturating mode go through C in scratch + requant_kernel.
+    Bit-exact against the numpy statement of the same arithmetic, per-column scales spanning the
+    clamp edges, with and without bias, several zero points, ragged N and output pitch."""
+    import torch
+    rng = np.random.default_rng(5 + mode)
+    for (m, n, k, ldo, zp, with_bias) in ((300, 333, 777, 340, 0, True), (2048, 1024, 1024, None, -3, False),
+                                          (16, 4096, 1024, None, 7, True), (129, 64, 640, 67, 0, True),
+                                          (257, 512, 2048, None, 1, True)):
+        a = oracle.mat_random_u8(m, k, m)
+        b = oracle.mat_random_i8(n, k, n)
+        scale = (rng.uniform(1.0 / 4000.0, 1.0 / 1000.0, n)).astype(np.float32)
+        bias = rng.integers(-200000, 200000, n, dtype=np.int32) if with_bias else None
+        ref = requant_ref(oracle.gemm(a, b, mode), scale, bias, zp)
+        ldo = n if ldo is None else ldo
+        dev = torch.device("cuda")
+        out = torch.full((m, ldo), 0x55, dtype=torch.int8, device=dev)[:, :n]
+        got = api.gemm_device_requant(torch.from_numpy(a).to(dev), torch.from_numpy(b).to(dev),
+                                      torch.from_numpy(scale).to(dev),
+                                      torch.from_numpy(bias).to(dev) if bias is not None else None, zp, out=out,
+                                      mode=mode)
+        torch.cuda.synchronize()
+        full = got.cpu().numpy()
+        assert (full == ref).all(), (mode, m, n, k, int((full != ref).sum()))
+        assert (ref == 127).any() and (ref == -128).any(), "the case should exercise both clamp edges"
+        pad = out.as_strided((m, ldo), (ldo, 1)).cpu().numpy()[:, n:]
+        assert (pad == 0x55).all(), "requant wrote outside the logical columns"
