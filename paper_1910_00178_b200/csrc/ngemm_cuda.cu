@@ -1391,7 +1391,9 @@ ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const i
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    if (sat_mode == NGEMM_SAT_EXACT && m > kSkinnyMaxM && m <= INT32_MAX - tc::BM && k <= INT32_MAX - tc::BK) {
+    const char* unfused = std::getenv("NGEMM_REQUANT_UNFUSED");  // experiments: time the unfused form
+    if (sat_mode == NGEMM_SAT_EXACT && m > kSkinnyMaxM && m <= INT32_MAX - tc::BM && k <= INT32_MAX - tc::BK &&
+        !(unfused && unfused[0] == '1')) {
         TcOps ops;
         ops.rq_scale = scale;
         ops.rq_bias = bias;
