@@ -107,8 +107,9 @@ ngemm_status ngemm_cuda_gemm_u8i8_strided_batched(const uint8_t* a, int64_t lda,
  *   out[r][c] = clamp(rint(float(C[r][c] + bias[c]) * scale[c]) + zero_point, -128, 127)
  * where C is the int32 GEMM of sat_mode, the int32 + bias add wraps, float(.) rounds to nearest,
  * the product is one IEEE fp32 multiply and rint rounds half to even.  scale: N floats (device),
- * bias: N int32 (device) or NULL.  Exact mode with M > 16 runs in the tcgen05 kernel's epilogue
- * (int32 C is never written to memory); other cases compute C in scratch and requantise it. */
+ * bias: N int32 (device) or NULL.  Exact mode requantises in the kernel's epilogue (tcgen05 for
+ * M > 16, the warp-MMA stream for M <= 16; int32 C is never written to memory); the saturating
+ * mode computes C in scratch and requantises it. */
 ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb,
                                           int8_t* out, int64_t ldo, int64_t m, int64_t n, int64_t k,
                                           const float* scale, const int32_t* bias, int zero_point,

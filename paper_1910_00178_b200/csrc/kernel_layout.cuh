@@ -102,9 +102,7 @@ __global__ void requant_kernel(const int32_t* __restrict__ c, int64_t ldc, int64
     for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < m * n;
          i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
         const int64_t r = i / n, col = i - r * n;
-        const uint32_t acc = static_cast<uint32_t>(c[r * ldc + col]) + static_cast<uint32_t>(bias ? bias[col] : 0);
-        const float prod = fminf(fmaxf(__fmul_rn(__int2float_rn(static_cast<int32_t>(acc)), scale[col]), -1.0e6f), 1.0e6f);
-        out[r * ldo + col] = static_cast<int8_t>(max(-128, min(127, __float2int_rn(prod) + zp)));
+        out[r * ldo + col] = requant_s8(static_cast<uint32_t>(c[r * ldc + col]), bias ? bias[col] : 0, scale[col], zp);
     }
 }
 

@@ -321,7 +321,7 @@ template <int MT, int RG, int WARPS>
 __global__ void __launch_bounds__(WARPS * 32)
     skinny_mma_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                       int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range,
-                      int vec_ok, int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc) {
+                      int vec_ok, int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc, Requant rq) {
     constexpr int KS = WARPS / RG;
     constexpr int NB = MT / 8;  // n8 blocks of A rows
     __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
@@ -443,6 +443,10 @@ __global__ void __launch_bounds__(WARPS * 32)
         for (int q = 0; q < KS; ++q) s += static_cast<uint32_t>(red[((r_g * KS + q) * 16 + row) * MT + m]);
         const int64_t n = (static_cast<int64_t>(blockIdx.x) * RG + r_g) * 16 + row;
         if (m < M && n < N) {
+            if (rq.out != nullptr) {  // fused requantisation (single K split only)
+                rq.out[static_cast<int64_t>(m) * rq.ldo + n] = requant_s8(s, rq.bias ? rq.bias[n] : 0, rq.scale[n], rq.zp);
+                continue;
+            }
             int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;
             if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
             else *dst = static_cast<int32_t>(s);

@@ -318,11 +318,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     for (int j = 0; j < 32; ++j) {
                         const float sj = __shfl_sync(0xffffffffu, my_s, j);
                         const int32_t bj = __shfl_sync(0xffffffffu, my_b, j);
-                        const float y = __int2float_rn(static_cast<int32_t>(v[j] + static_cast<uint32_t>(bj)));
-                        const float prod = fminf(fmaxf(__fmul_rn(y, sj), -1.0e6f), 1.0e6f);
-                        const int q = max(-128, min(127, __float2int_rn(prod) + map.rq_zp));
+                        const int8_t q = requant_s8(v[j], bj, sj, map.rq_zp);
                         if ((j & 3) == 0) packed[j >> 2] = 0;
-                        packed[j >> 2] |= (static_cast<uint32_t>(q) & 0xFFu) << (8 * (j & 3));
+                        packed[j >> 2] |= (static_cast<uint32_t>(static_cast<uint8_t>(q))) << (8 * (j & 3));
                     }
                     const int64_t row = static_cast<int64_t>(row0) + lane;
                     if (row < M) {

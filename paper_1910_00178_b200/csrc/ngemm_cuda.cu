@@ -462,8 +462,9 @@ int skinny_vec_flags(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb
 template <int MT, int WARPS, int RG = 1>
 ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                  int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
-                                 cudaStream_t st, const Batch& bt) {
+                                 cudaStream_t st, const Batch& bt, const Requant& rq = Requant()) {
     const int64_t groups = (n + 16 * RG - 1) / (16 * RG);
+    if (rq.out != nullptr) splits = 1;  // the requantised value needs the whole K sum
     const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
     splits = (k + k_range - 1) / k_range;
     for (int z = 0; z < bt.count && splits > 1; ++z) {
@@ -474,14 +475,14 @@ ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b,
     NG_LAUNCH(skinny_mma_kernel<MT, RG, WARPS>,
               dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
               dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
-              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
+              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc, rq);
     return NGEMM_OK;
 }
 
 template <int MT>
 ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                  int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
-                                 const Batch& bt = Batch()) {
+                                 const Batch& bt = Batch(), const Requant& rq = Requant()) {
     const int64_t groups = (n + 15) / 16 * bt.count;  // CTAs of all GEMMs of the batch fill the SMs
     const int64_t chunks = (k + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
     const int64_t warps_target = static_cast<int64_t>(di.sms) * 32;
@@ -508,13 +509,13 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
     // (16 x 768 x 3072: 4.6 -> 3.85 us, profiles/sweep_skinny_warps_r1.log)
     int64_t ks_use = MT >= 16 ? std::min<int64_t>(ks, 16) : ks;
     if (const char* f = std::getenv("NGEMM_SKINNY_WARPS")) ks_use = std::atoi(f);  // experiments: 8 / 16 / 32
-    if (rg == 2) return launch_skinny_mma_w<MT, 8, 2>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (rg == 4) return launch_skinny_mma_w<MT, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (rg == 8) return launch_skinny_mma_w<MT, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (ks_use <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (ks_use <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
-    if (ks > 32 && splits == 1) splits = (ks + 31) / 32;
-    return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    if (rg == 2) return launch_skinny_mma_w<MT, 8, 2>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
+    if (rg == 4) return launch_skinny_mma_w<MT, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
+    if (rg == 8) return launch_skinny_mma_w<MT, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
+    if (ks_use <= 8) return launch_skinny_mma_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
+    if (ks_use <= 16) return launch_skinny_mma_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
+    if (ks > 32 && splits == 1 && rq.out == nullptr) splits = (ks + 31) / 32;
+    return launch_skinny_mma_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
 }
 
 // Saturating load-stream variant (skinny_sat_kernel): 16 B-rows per CTA, 8/16/32 warps split
@@ -1402,7 +1403,17 @@ ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const i
         ops.rq_zp = zero_point;
         return launch_tcgen05(a, lda, b, ldb, nullptr, n, m, n, k, di, st, ops);
     }
-    // other shapes / the saturating mode: C in scratch, then the same arithmetic unfused
+    if (sat_mode == NGEMM_SAT_EXACT && m <= kSkinnyMaxM && !(unfused && unfused[0] == '1')) {
+        Requant rq;
+        rq.scale = scale;
+        rq.bias = bias;
+        rq.out = out;
+        rq.ldo = ldo;
+        rq.zp = zero_point;
+        return m <= 8 ? launch_skinny_mma_t<8>(a, lda, b, ldb, nullptr, n, m, n, k, di, st, Batch(), rq)
+                      : launch_skinny_mma_t<16>(a, lda, b, ldb, nullptr, n, m, n, k, di, st, Batch(), rq);
+    }
+    // the saturating mode: C in scratch, then the same arithmetic unfused
     int32_t* cbuf = nullptr;
     NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cbuf), static_cast<size_t>(m * n) * 4, st));
     s = run_gemm(a, lda, b, ldb, cbuf, n, m, n, k, sat_mode, NGEMM_KERNEL_AUTO, st);

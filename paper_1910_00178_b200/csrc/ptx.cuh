@@ -55,6 +55,23 @@ __device__ __forceinline__ bool elect_one() {
     return pred != 0;
 }
 
+// ---------------------------------------------------------------- requantisation
+// int8 = clamp(rint(float(acc + bias) * scale) + zp, -128, 127): the int32 add wraps, the
+// conversion rounds to nearest, one fp32 multiply, rint rounds half to even (ngemm_cuda.h).
+__device__ __forceinline__ int8_t requant_s8(uint32_t acc, int32_t bias, float scale, int zp) {
+    const float y = __int2float_rn(static_cast<int32_t>(acc + static_cast<uint32_t>(bias)));
+    const float prod = fminf(fmaxf(__fmul_rn(y, scale), -1.0e6f), 1.0e6f);
+    return static_cast<int8_t>(max(-128, min(127, __float2int_rn(prod) + zp)));
+}
+// Requantisation target passed to kernels (out == nullptr: plain int32 C).
+struct Requant {
+    const float* scale = nullptr;
+    const int32_t* bias = nullptr;  // may be null
+    int8_t* out = nullptr;
+    int64_t ldo = 0;
+    int zp = 0;
+};
+
 // ---------------------------------------------------------------- shared-window loads
 __device__ __forceinline__ uint4 lds_v4(uint32_t addr) {
     uint4 v;

@@ -68,7 +68,8 @@ void run(int m, int n, int k, int nbuf, int prefetch, int pdl, int ks_warps_log)
         const int vec = prefetch ? 3 : 1;
         CK(cudaLaunchKernelEx(&cfg, skinny_mma_kernel<MT, RG, 8>, (const uint8_t*)as[i % nbuf], (int64_t)k,
                               (const int8_t*)bs[i % nbuf], (int64_t)k, cs[i % nbuf], (int64_t)n, m, (int64_t)n,
-                              (int64_t)k, (int64_t)k, vec, 0, (int64_t)0, (int64_t)0, (int64_t)i));
+                              (int64_t)k, (int64_t)k, vec, 0, (int64_t)0, (int64_t)0, (int64_t)i,
+                              ngemm_dev::Requant()));
     };
     cudaGraph_t g;
     cudaGraphExec_t ge;

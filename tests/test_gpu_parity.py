@@ -558,15 +558,17 @@ def requant_ref(c, scale, bias, zp):
 
 @pytest.mark.parametrize("mode", [EXACT, SAT])
 def test_fused_requant_epilogue(cuda, oracle, mode):
-    """ngemm_cuda_gemm_u8i8_requant: exact mode, M > 16 requantises in the tcgen05 epilogue (int32
-    C never stored); M <= 16 and the saturating mode go through C in scratch + requant_kernel.
+    """ngemm_cuda_gemm_u8i8_requant: exact mode requantises in the kernel epilogue (tcgen05 for
+    M > 16, the warp-MMA stream for M <= 16; int32 C never stored); the saturating mode goes
+    through C in scratch + requant_kernel.
     Bit-exact against the numpy statement of the same arithmetic, per-column scales spanning the
     clamp edges, with and without bias, several zero points, ragged N and output pitch."""
     import torch
     rng = np.random.default_rng(5 + mode)
     for (m, n, k, ldo, zp, with_bias) in ((300, 333, 777, 340, 0, True), (2048, 1024, 1024, None, -3, False),
                                           (16, 4096, 1024, None, 7, True), (129, 64, 640, 67, 0, True),
-                                          (257, 512, 2048, None, 1, True)):
+                                          (257, 512, 2048, None, 1, True), (1, 768, 768, 770, 2, True),
+                                          (5, 333, 1001, None, 0, False)):
         a = oracle.mat_random_u8(m, k, m)
         b = oracle.mat_random_i8(n, k, n)
         scale = (rng.uniform(1.0 / 4000.0, 1.0 / 1000.0, n)).astype(np.float32)
