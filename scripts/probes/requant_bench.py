@@ -38,7 +38,8 @@ def timed(fn, reps, graph=True):
 
 dev = torch.device("cuda")
 l2 = torch.cuda.get_device_properties(dev).L2_cache_size
-for (m, n, k) in [(2048, 4096, 1024), (2048, 1024, 4096), (512, 4096, 1024), (1024, 1024, 1024), (8192, 8192, 8192)]:
+for (m, n, k) in [(2048, 4096, 1024), (2048, 1024, 4096), (512, 4096, 1024), (1024, 1024, 1024), (8192, 8192, 8192),
+                  (16, 4096, 1024), (4, 3072, 768), (1, 4096, 1024)]:
     per = m * k + n * k + 4 * m * n
     nb = 1 if per > 2 * l2 else min(16, int(4 * l2 // per) + 1)
     A = [torch.randint(0, 256, (m, k), dtype=torch.int32, device=dev).to(torch.uint8) for _ in range(nb)]
