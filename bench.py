@@ -424,6 +424,34 @@ def run_ours(args):
         v, cores, kind, sample, _ = cpu_reference_sample(a_h, b_h, N, K, mode)
         cpu = {"value": round(v, 5), "unit": "TOPS", "cores": cores, "kind": kind, "sample": sample}
 
+    # N > 1: the optional assembly of C on every rank (NCCL all-gather of the row shards over
+    # NVLink), timed separately from the GEMM; equal shards only.  A
+    # failure here is recorded, never fatal to the measurement above.
+    gather = None
+    if world > 1:
+        try:
+            import torch.distributed as dist
+            rows = [pdist.row_block(M, r, world, 128) for r in range(world)]
+            if all(r1 - r0 == mr for (r0, r1) in rows) and mr > 0:
+                full = torch.empty((world * mr, N), dtype=torch.int32, device=dev)
+                barrier(world)
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                dist.all_gather_into_tensor(full, cs[0])  # warm-up (NCCL channel setup)
+                torch.cuda.synchronize()
+                g0.record()
+                dist.all_gather_into_tensor(full, cs[0])
+                g1.record()
+                torch.cuda.synchronize()
+                g_ms = max_over_ranks(g0.elapsed_time(g1), world)
+                gbytes = world * mr * N * 4
+                gather = {"ms": round(g_ms, 4), "bytes_assembled_per_rank": gbytes,
+                          "GB_s_per_rank": round(gbytes / (g_ms * 1e-3) / 1e9, 1), "collective": "nccl all_gather"}
+                del full
+            else:
+                gather = {"skipped": "unequal row shards"}
+        except Exception as e:  # noqa: BLE001
+            gather = {"error": f"{type(e).__name__}: {e}"[:200]}
+
     if rank == 0:
         line = {
             "metric": "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T",
@@ -440,6 +468,8 @@ def run_ours(args):
             "kernel": picked, "gpu_launches": int(launches),
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
         }
+        if gather is not None:
+            line["gather"] = gather
         print(json.dumps(line), flush=True)
     if world > 1:
         import torch.distributed as dist
