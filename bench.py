@@ -4,19 +4,32 @@
 Headline workload (the largest single-GPU config, BASELINE.json configs[4]):
     c5  M = N = K = 16384, A uniform u8 [0,255], B uniform i8 [-128,127], exact int32
         (WideningExact, gemm_ref semantics); A sharded by rows over the ranks, B replicated.
-A step = one pass of the hot path (one GEMM of this rank's row block).  Inputs are
-synthetic, drawn on the device with seeded torch generators (shapes and value
-distributions of the config); A+B = 512 MiB > L2, so every step streams from HBM.
+A step = one pass of the hot path (one GEMM of this rank's row block).  Inputs are synthetic,
+drawn on the host with numpy's seeded PCG64 (seed 0 for A, 1 for B) — the SAME generator and
+seeds in both arms, so the reference arm measures the identical workload; A+B = 512 MiB > L2.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-                    [--config c5|c1|c2|c3|c4] [--mode exact|sat]
+                    [--config c5|c1|c4] [--shape MxNxK] [--mode exact|sat] [--no-shapes] ...
 
-Multi-GPU: launched under torch.distributed.run, one process per GPU (NCCL only for the
-barrier and the max-over-ranks of the timed region; the GEMM needs no collective).
-`--impl reference` times the reference's own CPU implementation (oracle/_ref: the
-unmodified header-only reference compiled from its sources; gemm_ref, the reference's only
-exact-mode kernel) on rank 0 with all host threads, on a bounded row sample of the same
-workload.
+One JSON line (rank 0).  Besides the contract keys it carries
+  * verified   — the timed C checked after the timed region: sampled row blocks bit-exact
+                 against the CPU oracle (the checker only) and, in exact mode, Freivalds rounds
+                 over the whole C on the device (bench.hpp:243-247: nothing unverified is timed);
+  * e2e        — the same metric through the C-ABI host entry with host buffers and the H2D/D2H
+                 copies inside the timed region; `variants` adds the pageable-memory call (what
+                 gemm_conventional on a MatrixBuf does) and the resident-weight call
+                 (gemm_ngemm's path: the packed weight stays in HBM, B in / C out per call);
+  * sustained  — 300 back-to-back steps (power-capped clock) next to the short burst;
+  * shapes     — every config-1..4 shape in both SatModes plus config 5 saturating: kernel,
+                 time, TOPS, roofline fraction, verified; CUDA-graph timed over rotating
+                 buffer sets totalling > 4x L2 (every launch L2-cold);
+  * cpu_baseline — the unmodified reference on ONE host core (primary: the reference is
+                 single-threaded) and on all cores (`all_cores`).
+Multi-GPU: one process per GPU under torch.distributed.run (NCCL only for the barrier, the
+max-over-ranks of the timed region and the optional, separately timed gather of C).
+`--impl reference` times the reference's own CPU implementation (oracle/_ref, the unmodified
+header-only reference compiled from its sources; gemm_ref for exact mode, gemm_conventional's
+native kernel for saturating mode) on rank 0 with all host threads, on a bounded row sample.
 """
 from __future__ import annotations
 
@@ -33,47 +46,93 @@ sys.path.insert(0, ROOT)
 
 SAT, EXACT = 0, 1
 INT8_PER_BF16 = 2.0  # int8 dense tensor rate = 2x bf16 (4.5 vs 2.25 PF nominal)
+DATASHEET_TOPS, SPEC_HBM_GBS = 4500.0, 8000.0
+METRIC = "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=50)
-    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--config", default="c5")
+    p.add_argument("--config", default="c5", choices=["c1", "c4", "c5"])
     p.add_argument("--mode", choices=["exact", "sat"], default="exact")
     p.add_argument("--shape", default=None, help="override MxNxK (sweeps)")
     p.add_argument("--kernel", default="auto", choices=["auto", "tcgen05", "simt", "skinny", "sat_hybrid"])
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--no-shapes", action="store_true", help="skip the per-shape sweep of configs 1-4")
+    p.add_argument("--no-sustained", action="store_true")
+    p.add_argument("--no-verify", action="store_true")
     p.add_argument("--eager", action="store_true", help="never capture a CUDA graph")
-    p.add_argument("--bdist", default="auto", choices=["auto", "uniform", "normal", "max", "min"],
-                   help="B distribution: uniform int8, or round(N(0, 32)) clipped (config 2's); "
-                        "auto = normal for M <= 16 (config 2), else uniform; max / min = all 127 / "
-                        "all -128 (config 4's extremes)")
-    p.add_argument("--adist", default="uniform", choices=["uniform", "max"],
-                   help="A distribution: uniform u8, or all 255 (config 4's extreme)")
+    p.add_argument("--bdist", default="auto", choices=["auto", "uniform", "normal", "max", "min", "alt"],
+                   help="B distribution: uniform int8, round(N(0, 32)) clipped (config 2's), or config 4's "
+                        "extremes (all 127 / all -128 / alternating -128,127); auto = normal for M <= 16")
+    p.add_argument("--adist", default="uniform", choices=["uniform", "max", "alt"],
+                   help="A distribution: uniform u8, or config 4's extremes (all 255 / alternating 0,255)")
     return p.parse_args()
 
 
-CONFIGS = {
-    "c1": (1024, 1024, 1024),
-    "c5": (16384, 16384, 16384),
-    "c4": (2048, 2048, 2048),
-}
+CONFIGS = {"c1": (1024, 1024, 1024), "c4": (2048, 2048, 2048), "c5": (16384, 16384, 16384)}
+NAMES = {"c1": "config1 single GEMM 1024^3", "c4": "config4 2048^3",
+         "c5": "config5 large GEMM 16384^3 (A row-sharded, B replicated)"}
 
 
 def workload(args):
     if args.shape:
         m, n, k = (int(x) for x in args.shape.lower().split("x"))
         return f"custom {m}x{n}x{k}", m, n, k
-    if args.config in CONFIGS:
-        m, n, k = CONFIGS[args.config]
-        names = {"c1": "config1 single GEMM 1024^3", "c5": "config5 large GEMM 16384^3 (A row-sharded, B replicated)",
-                 "c4": "config4 2048^3"}
-        return names[args.config], m, n, k
-    raise SystemExit(f"unknown config {args.config} (use --shape MxNxK for c2/c3 shapes)")
+    m, n, k = CONFIGS[args.config]
+    return NAMES[args.config], m, n, k
+
+
+# ------------------------------------------------------------------ synthetic inputs (both arms)
+def gen_a(rows, k, adist, seed=0):
+    import numpy as np
+    if adist == "max":
+        return np.full((rows, k), 255, np.uint8)
+    if adist == "alt":  # config 4: flat row-major index parity (idx & 1 ? 255 : 0)
+        return ((np.arange(rows * k, dtype=np.int64).reshape(rows, k) & 1) * 255).astype(np.uint8)
+    return np.random.default_rng(seed).integers(0, 256, (rows, k), dtype=np.uint8)
+
+
+def gen_b(n, k, bdist, seed=1):
+    import numpy as np
+    if bdist == "max":
+        return np.full((n, k), 127, np.int8)
+    if bdist == "min":
+        return np.full((n, k), -128, np.int8)
+    if bdist == "alt":  # idx & 1 ? 127 : -128
+        return np.where(np.arange(n * k, dtype=np.int64).reshape(n, k) & 1, 127, -128).astype(np.int8)
+    rng = np.random.default_rng(seed)
+    if bdist == "normal":  # config 2: round(N(0, sigma=32)) clipped to [-128, 127]
+        return np.clip(np.rint(rng.normal(0.0, 32.0, (n, k))), -128, 127).astype(np.int8)
+    return rng.integers(-128, 128, (n, k), dtype=np.int8)
+
+
+DIST_DESC = {"uniform_a": "uniform u8 [0,255]", "max_a": "all 255", "alt_a": "alternating 0/255",
+             "uniform": "uniform i8 [-128,127]", "normal": "round(N(0,32)) clipped to i8", "max": "all 127",
+             "min": "all -128", "alt": "alternating -128/127"}
+
+
+def resolve_bdist(args, m):
+    return ("normal" if m <= 16 else "uniform") if args.bdist == "auto" else args.bdist
+
+
+def data_desc(args, m):
+    return (f"synthetic: A {DIST_DESC[args.adist + '_a']}, B {DIST_DESC[resolve_bdist(args, m)]} "
+            f"(numpy PCG64, seed 0 for A and 1 for B, identical in both arms)")
+
+
+def config_dict(args, world):
+    """The workload description — identical in both arms (the driver compares them)."""
+    name, m, n, k = workload(args)
+    return {"workload": name, "M": m, "N": n, "K": k, "mode": args.mode,
+            "sat_semantics": "WideningExact (gemm_ref)" if args.mode == "exact" else
+            "HardwareSaturating (gemm_sat_oracle)",
+            "sharding": f"A rows over {world} rank(s), B replicated, no collective in the GEMM",
+            "l2": "operands larger than L2, or rotating buffer sets > 4x L2 (every launch L2-cold)"}
 
 
 def measured_peaks():
@@ -81,8 +140,9 @@ def measured_peaks():
     if os.path.exists(path):
         with open(path) as f:
             d = json.load(f)
-        return d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), "measured (MEASURED_PEAKS.json)"
-    return 6650.0, 1590.0, "fallback (B200_PROFILING.md)"
+        return (d.get("hbm_gbs", 6650.0), d.get("bf16_tflops", 1590.0), d.get("bf16_tflops_sustained"),
+                "measured (MEASURED_PEAKS.json)")
+    return 6650.0, 1590.0, None, "fallback (B200_PROFILING.md)"
 
 
 class ClockSampler:
@@ -155,7 +215,7 @@ class ClockSampler:
                 "samples": len(sm), "how": "nvidia-smi -lms 50, samples inside the timed region"}
 
 
-def dist_setup(args):
+def dist_setup():
     import torch
     import torch.distributed as dist
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -180,6 +240,10 @@ def max_over_ranks(x, world):
     return pdist.reduce_max(x, world, device="cuda")
 
 
+def min_over_ranks(x, world):
+    return -max_over_ranks(-float(x), world)
+
+
 def sum_over_ranks(x, world):
     from paper_1910_00178_b200 import dist as pdist
     return pdist.reduce_sum(x, world, device="cuda")
@@ -187,9 +251,8 @@ def sum_over_ranks(x, world):
 
 def load_traffic(tag):
     """Per-launch DRAM bytes of the dominant kernel from the committed ncu summary, if any."""
-    path = os.path.join(ROOT, "profiles", "traffic.json")
     try:
-        with open(path) as f:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
             return json.load(f).get(tag)
     except Exception:
         return None
@@ -221,13 +284,60 @@ def load_ncu(tag):
     return out
 
 
-def cpu_reference_sample(a_host, b_host, n, k, mode, target_s=12.0):
+def roofline_for(m, n, k, seconds, kernel):
+    """Roofline of one GEMM: algorithmic ops 2MNK and bytes MK + NK + 4MN (each operand read
+    once, C written once) against the measured peaks; `bound` follows the shape's ridge
+     for the tensor-core kernels, HBM otherwise."""
+    hbm_gbs, bf16_tf, _, basis = measured_peaks()
+    ops, nbytes = 2.0 * m * n * k, float(m * k + n * k + 4 * m * n)
+    tens_peak = bf16_tf * INT8_PER_BF16
+    tops = ops / seconds / 1e12
+    gbs = nbytes / seconds / 1e9
+    tensor = kernel in ("tcgen05", "sat_hybrid") and ops / (DATASHEET_TOPS * 1e12) > nbytes / (SPEC_HBM_GBS * 1e9)
+    if tensor:
+        r = {"bound": "tensor", "achieved": round(tops, 2), "peak": round(tens_peak, 1), "unit": "TOPS",
+             "frac": round(tops / tens_peak, 4)}
+    else:
+        r = {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_gbs, "unit": "GB/s", "frac": round(gbs / hbm_gbs, 4)}
+    r["frac_tensor"] = round(tops / tens_peak, 4)
+    r["frac_hbm"] = round(gbs / hbm_gbs, 4)
+    return r
+
+
+def verify_rows(dc, a_host, b_host, mode, r_lo, rows=64, blocks=2):
+    """Sampled row blocks of the device C (local rows) bit-exact against the CPU oracle."""
+    import numpy as np
+    from oracle.oracle import Oracle
+    ora = Oracle()
+    m = dc.shape[0]
+    starts = sorted({0, max(0, m - rows)} | ({max(0, (m // 2 // rows) * rows)} if blocks > 2 else set()))
+    bad = 0
+    checked = 0
+    for s in starts:
+        e = min(m, s + rows)
+        got = dc[s:e].cpu().numpy()
+        ref = ora.gemm(np.ascontiguousarray(a_host[r_lo + s:r_lo + e]), b_host, mode)
+        bad += int((got != ref).sum())
+        checked += e - s
+    return bad, checked
+
+
+def freivalds(dc, da, db, rounds=8, seed=7):
+    """C.x == A.(B^T.x) over the whole C in float64 with x in [0, 16): exact for |C| < 2^31 and
+    K <= 16384 (every partial sum an integer below 2^53).  Exact mode only."""
+    import torch
+    gen = torch.Generator(device=dc.device).manual_seed(seed)
+    x = torch.randint(0, 16, (dc.shape[1], rounds), device=dc.device, generator=gen).to(torch.float64)
+    lhs = dc.to(torch.float64) @ x
+    rhs = da.to(torch.float64) @ (db.to(torch.float64).t() @ x)
+    return bool(torch.equal(lhs, rhs))
+
+
+def cpu_reference_sample(a_host, b_host, n, k, mode, threads, target_s=8.0):
     """The reference's own CPU path on a bounded row sample of the workload: the unmodified
     reference compiled from its headers (oracle/_ref) when present, else our oracle port.
     Returns (value_TOPS, cores, kind, sample_desc, seconds)."""
-    import numpy as np
     from oracle.oracle import Oracle, Reference
-    threads = os.cpu_count() or 1
     m_total = a_host.shape[0]
     if Reference.available():
         ref = Reference()
@@ -258,74 +368,158 @@ def cpu_reference_sample(a_host, b_host, n, k, mode, target_s=12.0):
         rows = max(threads, rows // threads * threads) if rows < m_total else m_total
         dt = run(rows)
     ops = 2.0 * rows * n * k
-    return ops / dt / 1e12, threads, kind, f"{label}: rows 0..{rows} of A ({rows}x{n}x{k}) against all of B, " \
-                                          f"{threads} threads, {dt:.2f} s", dt
+    return ops / dt / 1e12, threads, kind, (f"{label}: rows 0..{rows} of A ({rows}x{n}x{k}) against all of B, "
+                                            f"{threads} thread(s), {dt:.2f} s"), dt
 
 
+# ------------------------------------------------------------------ per-shape sweep
+def sweep_cases():
+    """Every shape of BASELINE.json configs 1-4 in both SatModes, and config 5 saturating."""
+    cases = [("c1", 1024, 1024, 1024, "uniform", "uniform")]
+    for m in (1, 4, 16):
+        for (n, k) in ((768, 768), (3072, 768), (768, 3072), (4096, 1024)):
+            cases.append(("c2", m, n, k, "uniform", "normal"))
+    for m in (128, 512, 2048):
+        for (n, k) in ((1024, 1024), (4096, 1024), (1024, 4096)):
+            cases.append(("c3", m, n, k, "uniform", "uniform"))
+    for (m, n, k) in ((2048, 2048, 2048), (1000, 1000, 1000)):
+        for ad in ("max", "alt"):
+            for bd in ("min", "max", "alt"):
+                cases.append(("c4", m, n, k, ad, bd))
+    out = [(c, m, n, k, ad, bd, mode) for (c, m, n, k, ad, bd) in cases for mode in (EXACT, SAT)]
+    out.append(("c5", 16384, 16384, 16384, "uniform", "uniform", SAT))
+    return out
+
+
+def time_shape(dev, stream, m, n, k, mode, a_host, b_host, launches_min=20):
+    """Graph-timed device time per GEMM over rotating buffer sets (> 4x L2 of distinct bytes
+    between reuses, so every launch is L2-cold); returns (us, kernel, verified, launches, nbuf, gpu_launches)."""
+    import numpy as np
+    import torch
+    from oracle.oracle import Oracle
+    from paper_1910_00178_b200 import _lib, api
+    l2 = torch.cuda.get_device_properties(dev).L2_cache_size
+    per = m * k + n * k + 4 * m * n
+    nbuf = 1 if per > 2 * l2 else min(4096, int((4 * l2) // per) + 1)
+    launches = max(launches_min, nbuf) if per <= 2 * l2 else max(3, min(launches_min, int(2e10 // (2.0 * m * n * k)) + 3))
+    a0 = torch.from_numpy(a_host).to(dev)
+    b0 = torch.from_numpy(b_host).to(dev)
+    as_ = [a0] + [a0.clone() for _ in range(nbuf - 1)]
+    bs = [b0] + [b0.clone() for _ in range(nbuf - 1)]
+    cs = [torch.empty((m, n), dtype=torch.int32, device=dev) for _ in range(nbuf)]
+    kernel = api.pick_kernel(m, n, k, mode)
+    for i in range(min(nbuf, 3)):
+        api.gemm_device(as_[i], bs[i], cs[i], mode=mode, stream=stream)
+    torch.cuda.synchronize()
+    big = 2.0 * m * n * k > 2e11
+    graph = None
+    if not big:
+        graph = torch.cuda.CUDAGraph()
+        cap = torch.cuda.Stream(dev)
+        cap.wait_stream(stream)
+        with torch.cuda.stream(cap):
+            with torch.cuda.graph(graph, stream=cap):
+                for i in range(launches):
+                    api.gemm_device(as_[i % nbuf], bs[i % nbuf], cs[i % nbuf], mode=mode, stream=cap)
+        stream.wait_stream(cap)
+        graph.replay()
+        torch.cuda.synchronize()
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    n0 = _lib.launch_count()
+    ev0.record(stream)
+    if graph is not None:
+        graph.replay()
+    else:
+        for i in range(launches):
+            api.gemm_device(as_[i % nbuf], bs[i % nbuf], cs[i % nbuf], mode=mode, stream=stream)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    gl = _lib.launch_count() - n0 if graph is None else None
+    us = ev0.elapsed_time(ev1) * 1e3 / launches
+    # verification: the whole C when the oracle finishes fast, else sampled row blocks
+    ora = Oracle()
+    if 2.0 * m * n * k <= 1.5e10:
+        got = cs[0].cpu().numpy()
+        ok = bool((got == ora.gemm(a_host, b_host, mode)).all())
+        vdesc = "all of C vs oracle"
+    else:
+        rows = 16 if m * n * k > 2e11 else 64
+        bad, checked = verify_rows(cs[0], a_host, b_host, mode, 0, rows=rows, blocks=3)
+        ok = bad == 0
+        vdesc = f"{checked} rows of C (first/middle/last blocks) vs oracle"
+    del as_, bs, cs, graph
+    return us, kernel, ok, vdesc, launches, nbuf, gl
+
+
+def run_shapes(dev, stream):
+    out = []
+    for (cfg, m, n, k, ad, bd, mode) in sweep_cases():
+        a_host = gen_a(m, k, ad)
+        b_host = gen_b(n, k, bd)
+        try:
+            us, kernel, ok, vdesc, launches, nbuf, _ = time_shape(dev, stream, m, n, k, mode, a_host, b_host)
+        except Exception as e:  # noqa: BLE001 - record, keep sweeping
+            out.append({"config": cfg, "M": m, "N": n, "K": k, "mode": "exact" if mode == EXACT else "sat",
+                        "error": f"{type(e).__name__}: {e}"[:200]})
+            continue
+        rec = {"config": cfg, "M": m, "N": n, "K": k, "mode": "exact" if mode == EXACT else "sat",
+               "a": DIST_DESC[ad + "_a"], "b": DIST_DESC[bd], "kernel": kernel, "us": round(us, 3),
+               "value": round(2.0 * m * n * k / (us * 1e-6) / 1e12, 3), "unit": "TOPS",
+               "roofline": roofline_for(m, n, k, us * 1e-6, kernel), "verified": ok, "verify": vdesc,
+               "timing": (f"CUDA graph of {launches} launches over {nbuf} rotating buffer sets" if nbuf > 1 else
+                          f"{launches} launches, operands > L2")}
+        out.append(rec)
+    return out
+
+
+# ------------------------------------------------------------------ our arm
 def run_ours(args):
     import numpy as np
     import torch
     from paper_1910_00178_b200 import _lib, api
+    from paper_1910_00178_b200 import dist as pdist
 
-    rank, world, local = dist_setup(args)
+    rank, world, local = dist_setup()
     name, M, N, K = workload(args)
     mode = EXACT if args.mode == "exact" else SAT
     kernel = {"auto": _lib.KERNEL_AUTO, "tcgen05": _lib.KERNEL_TCGEN05, "simt": _lib.KERNEL_SIMT,
               "skinny": _lib.KERNEL_SKINNY, "sat_hybrid": _lib.KERNEL_SAT_HYBRID}[args.kernel]
-    from paper_1910_00178_b200 import dist as pdist
     r0, r1 = pdist.row_block(M, rank, world, 128)
     mr = r1 - r0
     dev = torch.device("cuda", local)
-
-    # synthetic inputs with the config's distributions, generated on the device
-    ga = torch.Generator(device=dev).manual_seed(0)
-    gb = torch.Generator(device=dev).manual_seed(1)
-    def make_a():
-        if args.adist == "max":  # config 4: all 255
-            return torch.full((max(mr, 1), K), 255, device=dev, dtype=torch.uint8)
-        return torch.randint(0, 256, (max(mr, 1), K), generator=ga, device=dev, dtype=torch.int32).to(torch.uint8)
-
-    a = make_a()
-    bnormal = args.bdist == "normal" or (args.bdist == "auto" and M <= 16)
-    b_desc = ("all %d" % (127 if args.bdist == "max" else -128) if args.bdist in ("max", "min") else
-              "round(N(0,32)) clipped to i8" if bnormal else "uniform i8 [-128,127]")
-    data_desc = ("synthetic: A " + ("all 255" if args.adist == "max" else "uniform u8 [0,255]") + ", B " + b_desc +
-                 " (torch generators seed 0/1, on device)")
-
-    def make_b():
-        if args.bdist in ("max", "min"):  # config 4's extremes
-            return torch.full((N, K), 127 if args.bdist == "max" else -128, device=dev, dtype=torch.int8)
-        if bnormal:  # config 2: round(N(0, sigma=32)) clipped to [-128, 127]
-            x = torch.randn((N, K), generator=gb, device=dev, dtype=torch.float32) * 32.0
-            return torch.clamp(torch.round(x), -128, 127).to(torch.int8)
-        return torch.randint(-128, 128, (N, K), generator=gb, device=dev, dtype=torch.int32).to(torch.int8)
-
-    b = make_b()
-    c = torch.empty((max(mr, 1), N), dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
+
+    # identical synthetic inputs in both arms (numpy PCG64, seeds 0 / 1); this rank's row block
+    a_full = gen_a(M, K, args.adist)
+    a_host = np.ascontiguousarray(a_full[r0:r1]) if mr > 0 else np.zeros((1, K), np.uint8)
+    b_host = gen_b(N, K, resolve_bdist(args, M))
+    a = torch.from_numpy(a_host).to(dev)
+    b = torch.from_numpy(b_host).to(dev)
+    c = torch.empty((max(mr, 1), N), dtype=torch.int32, device=dev)
     picked = _lib.KERNEL_NAMES[kernel] if kernel else api.pick_kernel(max(mr, 1), N, K, mode)
 
-    # small working sets: rotate distinct B/C buffers totalling > 4x L2 so every launch is L2-cold
+    # small working sets: rotate distinct A/B/C buffers totalling > 4x L2 so every launch is L2-cold
     l2 = torch.cuda.get_device_properties(dev).L2_cache_size
     per = (mr * K + N * K + 4 * mr * N)
-    nbuf = 1 if per > 2 * l2 else min(64, int((4 * l2) // max(per, 1)) + 1)
-    bs = [b] + [make_b() for _ in range(nbuf - 1)]
-    as_ = [a] + [make_a() for _ in range(nbuf - 1)]
+    nbuf = 1 if per > 2 * l2 else min(4096, int((4 * l2) // max(per, 1)) + 1)
+    nbuf = min(nbuf, max(1, args.steps))  # K launches touch K distinct sets (or rotate over > 4x L2)
+    steps = args.steps
+    flush = torch.empty(int(2 * l2), dtype=torch.uint8, device=dev) if nbuf > 1 else None
+    bs = [b] + [b.clone() for _ in range(nbuf - 1)]
+    as_ = [a] + [a.clone() for _ in range(nbuf - 1)]
     cs = [c] + [torch.empty_like(c) for _ in range(nbuf - 1)]
 
-    def step(i):
+    def step(i, st=stream):
         if mr > 0:
-            api.gemm_device(as_[i % nbuf], bs[i % nbuf], cs[i % nbuf], mode=mode, kernel=kernel, stream=stream)
+            api.gemm_device(as_[i % nbuf], bs[i % nbuf], cs[i % nbuf], mode=mode, kernel=kernel, stream=st)
 
     for i in range(args.warmup):
         step(i)
     torch.cuda.synchronize()
 
-    # Short GEMMs are captured into one CUDA graph (K launches over the rotating buffers) so
-    # the timed region measures the device, not Python/ctypes launch latency; long ones
-    # are launched eagerly.
+    # Short GEMMs are captured into one CUDA graph (K launches over the rotating buffers) so the
+    # timed region measures the device, not Python/ctypes launch latency; long ones run eagerly.
     use_graph = (2.0 * mr * N * K) < 2e11 and not args.eager
-    launches0 = _lib.launch_count()
     graph = None
     if use_graph:
         graph = torch.cuda.CUDAGraph()
@@ -333,15 +527,14 @@ def run_ours(args):
         cap.wait_stream(stream)
         with torch.cuda.stream(cap):
             with torch.cuda.graph(graph, stream=cap):
-                for i in range(args.steps):
-                    if mr > 0:
-                        api.gemm_device(as_[i % nbuf], bs[i % nbuf], cs[i % nbuf], mode=mode, kernel=kernel,
-                                        stream=cap)
+                for i in range(steps):
+                    step(i, cap)
         stream.wait_stream(cap)
         for _ in range(2):
             graph.replay()
         torch.cuda.synchronize()
-    launches = _lib.launch_count() - launches0
+    if flush is not None:  # L2 flushed before the timed region (the warm-up touched the same sets)
+        flush.zero_()
     barrier(world)
     torch.cuda.synchronize()
 
@@ -353,121 +546,123 @@ def run_ours(args):
         if graph is not None:
             graph.replay()
         else:
-            for i in range(args.steps):
+            for i in range(steps):
                 step(i)
         ev1.record(stream)
         torch.cuda.synchronize()
         clk.mark_end()
+    # kernels launched inside the timed region: counted at issue (eager) or at capture (graph:
+    # one library call per step, each launching the same kernels as the warm-up calls)
     if graph is None:
         launches = _lib.launch_count() - launches1
+    else:
+        n0 = _lib.launch_count()
+        step(0)
+        torch.cuda.synchronize()
+        launches = (_lib.launch_count() - n0) * steps
     barrier(world)
     torch.cuda.synchronize()
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
-    ms_step = ms / args.steps
+    ms_step = ms / steps
     total_ops = 2.0 * M * N * K
     value = total_ops / (ms_step * 1e-3) / 1e12  # TOPS, whole job
 
-    # dominant kernel: the GEMM itself (one launch per step); per-launch device time
-    kern_ms = ms_local / args.steps
-    hbm_gbs, bf16_tf, basis = measured_peaks()
-    alg_bytes = mr * K + N * K + 4 * mr * N
-    alg_ops = 2.0 * mr * N * K
-    tensor_bound = picked == "tcgen05" and (alg_ops / 4.5e15) > (alg_bytes / 8e12)
-    if tensor_bound:
-        peak = bf16_tf * INT8_PER_BF16
-        achieved = alg_ops / (kern_ms * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": round(peak, 1), "unit": "TOPS",
-                "frac": round(achieved / peak, 4),
-                "peak_basis": f"2 x bf16 dense tensor ({basis}: {bf16_tf} TF/s burst); datasheet 4500 TOPS",
-                "frac_of_datasheet": round(achieved / 4500.0, 4)}
-    else:
-        achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
-        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm_gbs, "unit": "GB/s",
-                "frac": round(achieved / hbm_gbs, 4), "peak_basis": basis}
+    # dominant kernel: the GEMM itself (one launch per step); per-launch device time on this rank
+    kern_s = ms_local / steps * 1e-3
+    roof = roofline_for(max(mr, 1), N, K, kern_s, picked)
+    hbm_gbs, bf16_tf, bf16_sus, basis = measured_peaks()
+    roof["peak_basis"] = (f"tensor: 2 x bf16 dense ({basis}: {bf16_tf} TF/s burst); datasheet {DATASHEET_TOPS:.0f} TOPS; "
+                          f"hbm: measured copy {hbm_gbs} GB/s")
+    roof["frac_of_datasheet"] = round(2.0 * mr * N * K / kern_s / 1e12 / DATASHEET_TOPS, 4)
     roof["traffic"] = load_traffic(f"{picked}:{mr}x{N}x{K}:{args.mode}")
     roof["ncu"] = load_ncu(f"{picked}:{mr}x{N}x{K}:{args.mode}")
-    roof["algorithmic_bytes_per_launch"] = alg_bytes
-    roof["algorithmic_ops_per_launch"] = alg_ops
+    roof["algorithmic_bytes_per_launch"] = mr * K + N * K + 4 * mr * N
+    roof["algorithmic_ops_per_launch"] = 2.0 * mr * N * K
     roof["kernel"] = picked
 
-    # e2e through the reference-facing host entry (pinned host A/B -> device -> C host)
+    # verification of the timed output (reference bench discipline: nothing unverified is timed)
+    verified = None
+    if not args.no_verify and mr > 0:
+        bad, checked = verify_rows(cs[0], a_full, b_host, mode, r0, rows=32 if mr * N * K > 1e11 else 128, blocks=3)
+        fr = freivalds(cs[0], as_[0], bs[0]) if mode == EXACT else None
+        ok_local = 1.0 if (bad == 0 and fr is not False) else 0.0
+        ok = min_over_ranks(ok_local, world) == 1.0
+        verified = ok
+        verify_desc = (f"rank {rank}: {checked} rows (first/middle/last blocks) bit-exact vs the CPU oracle" +
+                       ("; 8 Freivalds rounds (x in [0,16), float64) over the whole C" if mode == EXACT else ""))
+    else:
+        verify_desc = "skipped"
+
+    # sustained: 300 back-to-back steps (the int8 GEMM at full rate is power-capped on this part)
+    sustained = None
+    if not args.no_sustained and world == 1 and graph is None and mr > 0 and not args.shape:
+        n_sus = 300
+        with ClockSampler(local) as clk2:
+            clk2.mark_start()
+            ev0.record(stream)
+            for i in range(n_sus):
+                step(i)
+            ev1.record(stream)
+            torch.cuda.synchronize()
+            clk2.mark_end()
+        s_ms = ev0.elapsed_time(ev1) / n_sus
+        s_val = total_ops / (s_ms * 1e-3) / 1e12
+        sus_peak = (bf16_sus or bf16_tf) * INT8_PER_BF16
+        sustained = {"steps": n_sus, "value": round(s_val, 2), "ms_per_step": round(s_ms, 4),
+                     "frac_of_sustained_peak": round(s_val / sus_peak, 4), "sustained_peak": round(sus_peak, 1),
+                     "frac_of_datasheet": round(s_val / DATASHEET_TOPS, 4), "clocks": clk2.summary()}
+
+    # e2e through the reference-facing C-ABI host entries (host buffers, copies inside the region)
     e2e = None
     if not args.no_e2e:  # every rank takes part in the collectives, even one with no rows
-        L = _lib.load()
-        a_h = a.cpu().pin_memory()
-        b_h = b.cpu().pin_memory()
-        c_h = torch.empty((max(mr, 1), N), dtype=torch.int32).pin_memory()
-        e_steps = max(2, min(args.steps, 5 if M * N * K >= 1 << 40 else args.steps))
-
-        def host_call():
-            if mr > 0:
-                _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_h.data_ptr(), b_h.data_ptr(), c_h.data_ptr(), mr, N, K,
-                                                       mode, kernel))
-        for _ in range(min(2, args.warmup)):
-            host_call()
-        barrier(world)
-        t0 = time.perf_counter()
-        for _ in range(e_steps):
-            host_call()
-        dt = (time.perf_counter() - t0) / e_steps
-        dt = max_over_ranks(dt, world)
-        e2e = {"value": round(total_ops / dt / 1e12, 3), "unit": "TOPS", "ms_per_step": round(dt * 1e3, 3),
-               "h2d_bytes_per_step": int(sum_over_ranks(mr * K + N * K, world)),
-               "d2h_bytes_per_step": int(sum_over_ranks(4 * mr * N, world)),
-               "path": "ngemm_cuda_gemm_u8i8_host (C-ABI, pinned host buffers, synchronous)"}
+        e2e = run_e2e(args, world, mr, N, K, mode, kernel, a_host, b_host, as_[0], total_ops)
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        a_h = a.cpu().numpy()
-        b_h = b.cpu().numpy()
-        v, cores, kind, sample, _ = cpu_reference_sample(a_h, b_h, N, K, mode)
-        cpu = {"value": round(v, 5), "unit": "TOPS", "cores": cores, "kind": kind, "sample": sample}
+        v1, _, kind, sample1, _ = cpu_reference_sample(a_host, b_host, N, K, mode, threads=1, target_s=10.0)
+        threads = os.cpu_count() or 1
+        va, ca, _, samplea, _ = cpu_reference_sample(a_host, b_host, N, K, mode, threads=threads, target_s=8.0)
+        cpu = {"value": round(v1, 6), "unit": "TOPS", "cores": 1, "kind": kind, "sample": sample1,
+               "note": "primary baseline on 1 core: the reference is single-threaded by design (SPEC.md:303)",
+               "all_cores": {"value": round(va, 5), "unit": "TOPS", "cores": ca, "kind": kind, "sample": samplea,
+                             "harness": "rows of A sharded over std::threads (ours, not the reference's)"}}
+
+    timing_desc = (f"one CUDA graph of K launches over {nbuf} distinct buffer sets, L2 flushed before the region"
+                   if graph is not None and nbuf > 1 else
+                   "one CUDA graph of K launches, operands > L2" if graph is not None else
+                   "eager launches, operands > L2")
+    shapes = None
+    if rank == 0 and world == 1 and not args.no_shapes and not args.shape and args.config == "c5":
+        del as_, bs, cs, graph
+        torch.cuda.empty_cache()
+        shapes = run_shapes(dev, stream)
 
     # N > 1: the optional assembly of C on every rank (NCCL all-gather of the row shards over
-    # NVLink), timed separately from the GEMM; equal shards only.  A
-    # failure here is recorded, never fatal to the measurement above.
+    # NVLink), timed separately from the GEMM; equal shards only.  All ranks
+    # agree on success before entering the collective, so one rank's failure cannot hang the rest.
     gather = None
     if world > 1:
-        try:
-            import torch.distributed as dist
-            rows = [pdist.row_block(M, r, world, 128) for r in range(world)]
-            if all(r1 - r0 == mr for (r0, r1) in rows) and mr > 0:
-                full = torch.empty((world * mr, N), dtype=torch.int32, device=dev)
-                barrier(world)
-                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                dist.all_gather_into_tensor(full, cs[0])  # warm-up (NCCL channel setup)
-                torch.cuda.synchronize()
-                g0.record()
-                dist.all_gather_into_tensor(full, cs[0])
-                g1.record()
-                torch.cuda.synchronize()
-                g_ms = max_over_ranks(g0.elapsed_time(g1), world)
-                gbytes = world * mr * N * 4
-                gather = {"ms": round(g_ms, 4), "bytes_assembled_per_rank": gbytes,
-                          "GB_s_per_rank": round(gbytes / (g_ms * 1e-3) / 1e9, 1), "collective": "nccl all_gather"}
-                del full
-            else:
-                gather = {"skipped": "unequal row shards"}
-        except Exception as e:  # noqa: BLE001
-            gather = {"error": f"{type(e).__name__}: {e}"[:200]}
+        gather = run_gather(world, M, N, mr, c, dev, pdist)
 
     if rank == 0:
         line = {
-            "metric": "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T",
-            "value": round(value, 2), "unit": "TOPS", "n_gpus": world, "steps": args.steps,
+            "metric": METRIC,
+            "value": round(value, 2), "unit": "TOPS", "n_gpus": world, "steps": steps,
             "warmup": args.warmup, "ms_per_step": round(ms_step, 6), "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "u8*s8->s32",
-            "data": data_desc,
-            "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode,
-                       "sat_semantics": "WideningExact (gemm_ref)" if mode == EXACT else
-                       "HardwareSaturating (gemm_sat_oracle)",
-                       "sharding": f"A rows over {world} rank(s), B replicated, no collective",
-                       "l2": "inputs larger than L2" if nbuf == 1 else f"{nbuf} rotating buffer sets > 4x L2",
-                       "launch": "one CUDA graph of K launches" if graph is not None else "eager launches"},
+            "data": data_desc(args, M),
+            "config": config_dict(args, world),
+            "timing": timing_desc,
             "kernel": picked, "gpu_launches": int(launches),
+            "verified": verified, "verify": verify_desc,
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk.summary(),
         }
+        if sustained is not None:
+            line["sustained"] = sustained
+        if shapes is not None:
+            line["shapes"] = shapes
+            line["shapes_verified"] = all(s.get("verified") is True for s in shapes)
         if gather is not None:
             line["gather"] = gather
         print(json.dumps(line), flush=True)
@@ -476,27 +671,121 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def run_e2e(args, world, mr, N, K, mode, kernel, a_host, b_host, a_dev, total_ops):
+    """e2e: the same metric through the C-ABI host entries, H2D and D2H inside the timed region.
+    Primary: ngemm_cuda_gemm_u8i8_host on pinned host A/B/C.  Variants: the same call on pageable
+    (numpy) buffers — what gemm_conventional on a MatrixBuf does — and the resident-weight call
+    of gemm_ngemm (ngemm_cuda_gemm_packed_resident_host: the weight A stays in HBM, B in and C
+    out per call)."""
+    import numpy as np
+    import torch
+    from paper_1910_00178_b200 import _lib
+    L = _lib.load()
+    big = mr * N * K >= 1 << 40
+    e_steps = max(2, min(args.steps, 5 if big else args.steps))
+
+    def timed(fn):
+        for _ in range(min(2, max(1, args.warmup))):
+            fn()
+        barrier(world)
+        t0 = time.perf_counter()
+        for _ in range(e_steps):
+            fn()
+        return max_over_ranks((time.perf_counter() - t0) / e_steps, world)
+
+    def rec(dt, h2d, d2h, path):
+        return {"value": round(total_ops / dt / 1e12, 3), "unit": "TOPS", "ms_per_step": round(dt * 1e3, 3),
+                "h2d_bytes_per_step": int(sum_over_ranks(h2d, world)),
+                "d2h_bytes_per_step": int(sum_over_ranks(d2h, world)), "path": path}
+
+    a_p = torch.from_numpy(a_host).pin_memory()
+    b_p = torch.from_numpy(b_host).pin_memory()
+    c_p = torch.empty((max(mr, 1), N), dtype=torch.int32).pin_memory()
+
+    def pinned():
+        if mr > 0:
+            _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_p.data_ptr(), b_p.data_ptr(), c_p.data_ptr(), mr, N, K, mode,
+                                                   kernel))
+    out = rec(timed(pinned), mr * K + N * K, 4 * mr * N,
+              "ngemm_cuda_gemm_u8i8_host (C-ABI, pinned host A/B/C, synchronous per call)")
+    variants = {}
+    c_np = np.empty((max(mr, 1), N), np.int32)
+
+    def pageable():
+        if mr > 0:
+            _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_host.ctypes.data, b_host.ctypes.data, c_np.ctypes.data, mr, N, K,
+                                                   mode, kernel))
+    variants["pageable"] = rec(timed(pageable), mr * K + N * K, 4 * mr * N,
+                               "ngemm_cuda_gemm_u8i8_host on pageable host memory (gemm_conventional on MatrixBufs)")
+    if mr > 0:
+        import ctypes as C
+        h = C.c_void_p()
+        _lib.check(L.ngemm_cuda_packed_from_device(a_dev.data_ptr(), a_dev.stride(0), mr, K, C.byref(h)))
+
+        def resident():
+            _lib.check(L.ngemm_cuda_gemm_packed_resident_host(h, b_p.data_ptr(), c_p.data_ptr(), N, mode))
+        try:
+            variants["resident_weight"] = rec(timed(resident), N * K, 4 * mr * N,
+                                              "ngemm_cuda_gemm_packed_resident_host (gemm_ngemm: weight A resident "
+                                              "in HBM; pinned B in, pinned C out per call)")
+        finally:
+            L.ngemm_cuda_packed_free(h)
+    else:
+        timed(lambda: None)
+    if mr > 0:  # the pinned call's C must be the device result
+        ok = bool(np.array_equal(c_p[:64].numpy(), c_np[:64]))
+        out["checked"] = ok
+    out["variants"] = variants
+    return out
+
+
+def run_gather(world, M, N, mr, c, dev, pdist):
+    import torch
+    import torch.distributed as dist
+    rows = [pdist.row_block(M, r, world, 128) for r in range(world)]
+    if not (all(r1 - r0 == mr for (r0, r1) in rows) and mr > 0):
+        return {"skipped": "unequal row shards"}
+    full, err = None, None
+    try:
+        full = torch.empty((world * mr, N), dtype=torch.int32, device=dev)
+    except Exception as e:  # noqa: BLE001
+        err = f"{type(e).__name__}: {e}"[:200]
+    ok = min_over_ranks(1.0 if full is not None else 0.0, world) == 1.0
+    if not ok:
+        return {"error": err or "allocation failed on another rank"}
+    barrier(world)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    dist.all_gather_into_tensor(full, c)  # warm-up (NCCL channel setup)
+    torch.cuda.synchronize()
+    g0.record()
+    dist.all_gather_into_tensor(full, c)
+    g1.record()
+    torch.cuda.synchronize()
+    g_ms = max_over_ranks(g0.elapsed_time(g1), world)
+    gbytes = world * mr * N * 4
+    del full
+    return {"ms": round(g_ms, 4), "bytes_assembled_per_rank": gbytes,
+            "GB_s_per_rank": round(gbytes / (g_ms * 1e-3) / 1e9, 1), "collective": "nccl all_gather"}
+
+
+# ------------------------------------------------------------------ reference arm
 def run_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     if rank != 0:
         return
-    import numpy as np
     from oracle.oracle import Oracle, Reference
     name, M, N, K = workload(args)
     mode = EXACT if args.mode == "exact" else SAT
-    ora = Oracle()
-    # same distributions as our arm (host-side seeded draws; the reference has its own PRNG)
-    rng = np.random.default_rng(0)
     threads = os.cpu_count() or 1
     # bounded sample: rows sized so each step takes ~min(3 s, 100 s / (steps + warmup)) on all
     # host threads, keeping the whole reference run within a few minutes
     step_s = min(3.0, 100.0 / max(1, args.steps + args.warmup))
-    b = rng.integers(-128, 128, (N, K), dtype=np.int8)
-    a_probe = rng.integers(0, 256, (min(M, threads), K), dtype=np.uint8)
-    _, _, kind, _, dt = cpu_reference_sample(a_probe, b, N, K, mode, target_s=0.0)
+    a_full = gen_a(M, K, args.adist)  # the same generator and seeds as our arm
+    b = gen_b(N, K, resolve_bdist(args, M))
+    _, _, kind, _, dt = cpu_reference_sample(a_full[:min(M, threads)], b, N, K, mode, threads, target_s=0.0)
     rows = min(M, max(threads, int(threads * step_s / max(dt, 1e-3)) // threads * threads))
-    a = rng.integers(0, 256, (rows, K), dtype=np.uint8)
+    a = a_full[:rows]
     variant = "gemm_ref" if mode == EXACT else "gemm_conventional"
     if Reference.available():
         ref = Reference()
@@ -504,6 +793,7 @@ def run_reference(args):
         run = sess.run
         label = f"{variant} (oracle/_ref unmodified reference, host_isa={ref.host_isa_bits()} bit)"
     else:
+        ora = Oracle()
         run = lambda: ora.gemm(a, b, mode, threads=threads)  # noqa: E731
         label = "oracle port (oracle/oracle.c)"
     for _ in range(args.warmup):
@@ -516,11 +806,11 @@ def run_reference(args):
     sample = f"{label}: rows 0..{rows} of A ({rows}x{N}x{K}) against all of B per step, {threads} threads"
     line = {
         "impl": "reference",
-        "metric": "int8 GEMM TOPS (2*M*N*K/s), C[i32] = A[u8] * B[i8]^T",
+        "metric": METRIC,
         "value": round(value, 5), "unit": "TOPS", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(dt * 1e3, 3), "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "u8*s8->s32", "data": "synthetic: A uniform u8 [0,255], B uniform i8 [-128,127] (numpy seed 0)",
-        "config": {"workload": name, "M": M, "N": N, "K": K, "mode": args.mode},
+        "dtype": "u8*s8->s32", "data": data_desc(args, M),
+        "config": config_dict(args, world),
         "cpu_baseline": {"value": round(value, 5), "unit": "TOPS", "cores": threads, "kind": kind, "sample": sample},
         "e2e": {"value": round(value, 5), "unit": "TOPS", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }

@@ -135,8 +135,8 @@ inline MatrixBuf gemm_ngemm(const PackedWeight& p, const MatrixBuf& b, SatMode m
     MatrixBuf c(ElemKind::I32, p.m_orig(), b.rows());
     const ngemm_packed_meta meta = p.meta();
     if (kernel == NGEMM_KERNEL_AUTO && p.kind() == ElemKind::U8) {
-        const DeviceWeight& w = p.device_weight();
-        throw_on_status(ngemm_cuda_gemm_packed_resident_host(w.handle(), b.row<std::int8_t>(0),
+        const std::shared_ptr<const DeviceWeight> w = p.device_weight();  // held for the whole call
+        throw_on_status(ngemm_cuda_gemm_packed_resident_host(w->handle(), b.row<std::int8_t>(0),
                                                              c.row<std::int32_t>(0), b.rows(), detail::abi_mode(mode)));
     } else {
         throw_on_status(ngemm_cuda_gemm_packed_host(&meta, p.bytes(), p.byte_size(), b.bytes(),

@@ -202,6 +202,21 @@ ngemm_status ngemm_cuda_tune_store_save(const char* path);
 ngemm_status ngemm_cuda_tune_store_load(const char* path, int* loaded);
 ngemm_status ngemm_cuda_tune_clear(void);
 
+/* ---- experiment / test knobs and the scratch pool ---------------------------------------
+ * Kernel-selection overrides used by the tests and sweep scripts (never needed in production):
+ * PDL, L2_PREFETCH, SKINNY_FAST, SKINNY_SPLITS, SKINNY_RG, SKINNY_WARPS, SKINNY_VARIANT, TC_QUAD,
+ * TC_CFG, TC_SPLITS, TC_DIRECT, TC_PREISSUE, TC_L2HINT, TC_GROUP_M, TC_DBG, SAT_HYBRID,
+ * SATFIX_SKIP, I16_PATH (1 tcgen05 / 0 simt), REQUANT_UNFUSED, TC_SCHED; -1 = unset.  Initial
+ * values are read ONCE from NGEMM_<NAME> environment variables; the launch path never reads the
+ * environment.  Names may carry the NGEMM_ prefix.  get_option returns INT32_MIN for an unknown
+ * name; reset_options re-reads the environment. */
+ngemm_status ngemm_cuda_set_option(const char* name, int value);
+int ngemm_cuda_get_option(const char* name);
+ngemm_status ngemm_cuda_reset_options(void);
+/* Scratch buffers come from a private stream-ordered pool per device (the device's default pool
+ * is never reconfigured); trim returns the current device's cached scratch to the driver. */
+ngemm_status ngemm_cuda_trim(void);
+
 /* ---- introspection ----------------------------------------------------------------------- */
 /* Current CUDA device of the calling thread. */
 ngemm_status ngemm_cuda_device(int* device);

@@ -22,7 +22,8 @@ EXPORTS = [
     "ngemm_cuda_launch_count", "ngemm_cuda_gemm_i16", "ngemm_cuda_gemm_i16_host", "ngemm_cuda_gemm_packed_i16",
     "ngemm_cuda_gemm_packed_resident_host", "ngemm_cuda_device", "ngemm_cuda_tune", "ngemm_cuda_tune_store_save",
     "ngemm_cuda_tune_store_load", "ngemm_cuda_tune_clear", "ngemm_cuda_gemm_u8i8_strided_batched",
-    "ngemm_cuda_gemm_u8i8_requant",
+    "ngemm_cuda_gemm_u8i8_requant", "ngemm_cuda_set_option", "ngemm_cuda_get_option", "ngemm_cuda_reset_options",
+    "ngemm_cuda_trim",
 ]
 
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA, ERR_TUNE = range(9)
@@ -88,10 +89,14 @@ def load():
         L.ngemm_cuda_tune_store_save.argtypes = [C.c_char_p]
         L.ngemm_cuda_tune_store_load.argtypes = [C.c_char_p, C.POINTER(i32)]
         L.ngemm_cuda_tune_clear.argtypes = []
+        L.ngemm_cuda_set_option.argtypes = [C.c_char_p, i32]
+        L.ngemm_cuda_get_option.argtypes = [C.c_char_p]
+        L.ngemm_cuda_reset_options.argtypes = []
+        L.ngemm_cuda_trim.argtypes = []
         for f in EXPORTS:
             fn = getattr(L, f)
             if f not in ("ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error",
-                         "ngemm_cuda_pick_kernel", "ngemm_cuda_launch_count"):
+                         "ngemm_cuda_pick_kernel", "ngemm_cuda_launch_count", "ngemm_cuda_get_option"):
                 fn.restype = st
         L.ngemm_cuda_abi_version.restype = C.c_int
         L.ngemm_cuda_status_name.argtypes = [C.c_int]
@@ -100,6 +105,7 @@ def load():
         L.ngemm_cuda_pick_kernel.argtypes = [i64, i64, i64, i32]
         L.ngemm_cuda_pick_kernel.restype = C.c_int
         L.ngemm_cuda_launch_count.restype = C.c_uint64
+        L.ngemm_cuda_get_option.restype = C.c_int
         _lib = L
         return L
 
@@ -154,3 +160,34 @@ def check(status: int):
 
 def launch_count() -> int:
     return int(load().ngemm_cuda_launch_count())
+
+
+def set_option(name: str, value: int):
+    """Experiment / test knob (include/ngemm_cuda.h): e.g. set_option("TC_CFG", 2)."""
+    check(load().ngemm_cuda_set_option(name.encode(), int(value)))
+
+
+def get_option(name: str) -> int:
+    return int(load().ngemm_cuda_get_option(name.encode()))
+
+
+def reset_options():
+    check(load().ngemm_cuda_reset_options())
+
+
+class options:
+    """Context manager: `with _lib.options(TC_CFG=2, TC_SPLITS=1): ...` restores the knobs after."""
+
+    def __init__(self, **kv):
+        self.kv = kv
+        self.saved = {}
+
+    def __enter__(self):
+        for k, v in self.kv.items():
+            self.saved[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *exc):
+        for k, v in self.saved.items():
+            set_option(k, v)

@@ -267,13 +267,23 @@ def gemm_device_requant(a, b, scale, bias=None, zero_point: int = 0, out=None,
         raise UnsupportedError(f"gemm: no kernel path for {a.dtype} x {b.dtype}")
     if a.dim() != 2 or b.dim() != 2 or a.shape[1] != b.shape[1]:
         raise ShapeError(f"gemm: K mismatch, A is {tuple(a.shape)} but B is {tuple(b.shape)}")
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise ShapeError("gemm: operands must be K-contiguous")
     m, k = a.shape
     n = b.shape[0]
-    if scale.dtype != torch.float32 or scale.shape != (n,) or (bias is not None and
-                                                             (bias.dtype != torch.int32 or bias.shape != (n,))):
+    if scale.dtype != torch.float32 or tuple(scale.shape) != (n,) or (bias is not None and
+                                                                    (bias.dtype != torch.int32 or
+                                                                     tuple(bias.shape) != (n,))):
         raise ShapeError("requant: scale must be float32 [N] and bias int32 [N]")
+    if not scale.is_contiguous() or (bias is not None and not bias.is_contiguous()):
+        raise ShapeError("requant: scale and bias must be contiguous")
+    for t in (b, scale) + ((bias,) if bias is not None else ()):
+        if t.device != a.device:
+            raise ShapeError(f"requant: operands must live on {a.device}, got one on {t.device}")
     if out is None:
         out = torch.empty((m, n), dtype=torch.int8, device=a.device)
+    if out.dtype != torch.int8 or tuple(out.shape) != (m, n) or out.stride(1) != 1 or out.device != a.device:
+        raise ShapeError("requant: out must be int8 [M, N] with unit column stride on A's device")
     check(_lib.load().ngemm_cuda_gemm_u8i8_requant(
         a.data_ptr(), a.stride(0), b.data_ptr(), b.stride(0), out.data_ptr(), out.stride(0), m, n, k,
         scale.data_ptr(), bias.data_ptr() if bias is not None else None, int(zero_point), int(mode),

@@ -110,25 +110,98 @@ DevInfo dev_info(int dev) {
     return d;
 }
 
-// Keep freed stream-ordered allocations cached in the device pool (the default release
-// threshold of 0 would return them to the OS at every synchronisation, turning each
-// host-entry call into a fresh multi-GB mapping).
-void keep_pool(int dev) {
-    static std::once_flag once[64];
-    std::call_once(once[dev & 63], [dev] {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+// ---------------------------------------------------------------- experiment / test knobs
+// Read ONCE from the environment (NGEMM_<NAME>) on first use and never again on the launch
+// path; tests and the sweep scripts change them through ngemm_cuda_set_option.  -1 = unset
+// (the planner decides).  None of them is needed in production.
+enum Opt : int {
+    O_PDL, O_L2_PREFETCH, O_SKINNY_FAST, O_SKINNY_SPLITS, O_SKINNY_RG, O_SKINNY_WARPS, O_SKINNY_VARIANT,
+    O_TC_QUAD, O_TC_CFG, O_TC_SPLITS, O_TC_DIRECT, O_TC_PREISSUE, O_TC_L2HINT, O_TC_GROUP_M, O_TC_DBG,
+    O_SAT_HYBRID, O_SATFIX_SKIP, O_I16_PATH, O_REQUANT_UNFUSED, O_TC_SCHED, O_N
+};
+struct OptDef {
+    const char* name;
+    int def;
+};
+constexpr OptDef kOpts[O_N] = {
+    {"PDL", 1}, {"L2_PREFETCH", 1}, {"SKINNY_FAST", 1}, {"SKINNY_SPLITS", -1}, {"SKINNY_RG", -1},
+    {"SKINNY_WARPS", -1}, {"SKINNY_VARIANT", -1}, {"TC_QUAD", 0}, {"TC_CFG", -1}, {"TC_SPLITS", -1},
+    {"TC_DIRECT", 0}, {"TC_PREISSUE", 0}, {"TC_L2HINT", 3}, {"TC_GROUP_M", -1}, {"TC_DBG", 0},
+    {"SAT_HYBRID", -1}, {"SATFIX_SKIP", 0}, {"I16_PATH", -1}, {"REQUANT_UNFUSED", 0}, {"TC_SCHED", -1},
+};
+std::atomic<int> g_opt[O_N];
+std::once_flag g_opt_once;
+
+int env_opt(int i) {
+    const std::string key = std::string("NGEMM_") + kOpts[i].name;
+    const char* e = std::getenv(key.c_str());
+    if (!e || !*e) return kOpts[i].def;
+    if (i == O_I16_PATH) return std::strcmp(e, "tcgen05") == 0 ? 1 : 0;  // "tcgen05" | "simt"
+    return std::atoi(e);
+}
+void load_opts() {
+    for (int i = 0; i < O_N; ++i) g_opt[i].store(env_opt(i), std::memory_order_relaxed);
+}
+int opt(Opt o) {
+    std::call_once(g_opt_once, load_opts);
+    return g_opt[o].load(std::memory_order_relaxed);
+}
+int opt_index(const char* name) {
+    if (!name) return -1;
+    if (std::strncmp(name, "NGEMM_", 6) == 0) name += 6;
+    for (int i = 0; i < O_N; ++i)
+        if (std::strcmp(name, kOpts[i].name) == 0) return i;
+    return -1;
+}
+
+// Stream-ordered scratch comes from the library's OWN pool per device (release threshold
+// UINT64_MAX, so a host-entry call does not remap multi-GB buffers every time); the device's
+// default pool — shared with the host application — is left untouched.  ngemm_cuda_trim()
+// returns the cached bytes.  Inside a stream capture the allocation becomes a graph node.
+cudaMemPool_t lib_pool(int dev) {
+    static std::mutex mu;
+    static cudaMemPool_t pools[64] = {};
+    static bool made[64] = {};
+    if (dev < 0 || dev >= 64) return nullptr;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!made[dev]) {
+        made[dev] = true;
+        cudaMemPoolProps props = {};
+        props.allocType = cudaMemAllocationTypePinned;
+        props.location.type = cudaMemLocationTypeDevice;
+        props.location.id = dev;
+        if (cudaMemPoolCreate(&pools[dev], &props) == cudaSuccess) {
             uint64_t thr = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+            cudaMemPoolSetAttribute(pools[dev], cudaMemPoolAttrReleaseThreshold, &thr);
+        } else {
+            cudaGetLastError();
+            pools[dev] = nullptr;
         }
-    });
+    }
+    return pools[dev];
+}
+
+cudaError_t dev_alloc(void** p, size_t bytes, cudaStream_t st) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        return cudaMallocAsync(p, bytes, st);
+    }
+    if (cs != cudaStreamCaptureStatusNone) return cudaMallocAsync(p, bytes, st);  // graph allocation node
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool = lib_pool(dev);
+    return pool ? cudaMallocFromPoolAsync(p, bytes, pool, st) : cudaMallocAsync(p, bytes, st);
+}
+template <typename T>
+cudaError_t dev_alloc(T** p, size_t bytes, cudaStream_t st) {
+    return dev_alloc(reinterpret_cast<void**>(p), bytes, st);
 }
 
 void autoload_tune_store();
 
 ngemm_status current_device(int* dev, DevInfo* info) {
     NG_CUDA(cudaGetDevice(dev));
-    keep_pool(*dev);
     autoload_tune_store();
     *info = dev_info(*dev);
     if (info->sms <= 0) return fail(NGEMM_ERR_CUDA, "no CUDA device");
@@ -218,13 +291,7 @@ struct Batch {
 // launch and prologue (barrier init, TMEM alloc, descriptor prefetch) with the tail of the
 // previous one; every kernel calls griddepcontrol.wait before touching global memory, so
 // stream order semantics are unchanged.  NGEMM_PDL=0 disables it.
-bool pdl_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NGEMM_PDL");
-        return !(e && e[0] == '0');
-    }();
-    return on;
-}
+bool pdl_enabled() { return opt(O_PDL) != 0; }
 
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, unsigned cx,
@@ -373,7 +440,7 @@ ngemm_status stage_tma_operands(const uint8_t*& a, int64_t& lda, int64_t m, cons
     if (a_ok && b_ok) return NGEMM_OK;
     const int64_t kp = round_up(k, 16);
     const int64_t ma = a_ok ? 0 : m, nb = b_ok ? 0 : n;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(scratch), static_cast<size_t>((ma + nb) * kp), st));
+    NG_CUDA(dev_alloc(scratch, static_cast<size_t>((ma + nb) * kp), st));
     uint8_t* da = *scratch;
     uint8_t* db = *scratch + ma * kp;
     int dev = 0;
@@ -412,13 +479,16 @@ ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, in
     int64_t lda_use = lda, ldb_use = ldb;
     uint8_t* scratch = nullptr;
     s = stage_tma_operands(a_use, lda_use, m, b_use, ldb_use, n, k, &scratch, st);
-    if (s != NGEMM_OK) return s;
+    if (s != NGEMM_OK) {
+        if (scratch) cudaFreeAsync(scratch, st);
+        return s;
+    }
     const int n_tiles = static_cast<int>((n + tcs::BN_ROWS - 1) / tcs::BN_ROWS);
     const int num_kb = static_cast<int>((k + tcs::BK - 1) / tcs::BK);
     // cluster size along K: a power of two <= 8 (so 128 divides evenly), enough CTAs for ~2 waves
     // about one CTA per SM, each streaming several K blocks (measured best on the c2 shapes)
     int want = std::max(1, (di.sms + n_tiles - 1) / n_tiles);
-    if (const char* f = std::getenv("NGEMM_SKINNY_SPLITS")) want = std::max(1, std::atoi(f));
+    if (opt(O_SKINNY_SPLITS) > 0) want = opt(O_SKINNY_SPLITS);
     int ks = 1;
     while (ks * 2 <= std::min(8, std::min(want, num_kb))) ks *= 2;
     const int kb_per = (num_kb + ks - 1) / ks;
@@ -441,21 +511,12 @@ ngemm_status launch_tc_skinny(const uint8_t* a, int64_t lda, const int8_t* b, in
 // Skinny kernels' `vec_ok` argument: bit 0 = operands allow 16-byte vector loads, bit 1 = also
 // warm L2 with the CTA's operand rows before the PDL dependency wait (NGEMM_L2_PREFETCH=0 off),
 // bit 2 = whole in-range chunks take the branch-free load path (NGEMM_SKINNY_FAST=0 off).
-bool l2_prefetch_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("NGEMM_L2_PREFETCH");
-        return !(e && std::atoi(e) == 0);
-    }();
-    return on;
-}
+bool l2_prefetch_enabled() { return opt(O_L2_PREFETCH) != 0; }
 
 int skinny_vec_flags(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, const Batch& bt) {
     const bool vec = reinterpret_cast<uintptr_t>(b) % 16 == 0 && ldb % 16 == 0 &&
                      reinterpret_cast<uintptr_t>(a) % 16 == 0 && lda % 16 == 0 && bt.sa % 16 == 0 && bt.sb % 16 == 0;
-    static const bool fast = [] {
-        const char* e = std::getenv("NGEMM_SKINNY_FAST");
-        return !(e && std::atoi(e) == 0);
-    }();
+    const bool fast = opt(O_SKINNY_FAST) != 0;
     return vec ? (1 | (l2_prefetch_enabled() ? 2 : 0) | (fast ? 4 : 0)) : 0;
 }
 
@@ -488,7 +549,7 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
     const int64_t warps_target = static_cast<int64_t>(di.sms) * 32;
     const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (warps_target + groups - 1) / groups));
     int64_t splits = 1;
-    if (const char* f = std::getenv("NGEMM_SKINNY_SPLITS")) splits = std::max(1, std::atoi(f));
+    if (opt(O_SKINNY_SPLITS) > 0) splits = opt(O_SKINNY_SPLITS);
     // Row groups per CTA (RG, 8 warps): a single skinny GEMM has too few 16-row groups to fill
     // 148 SMs, so RG = 1 and the warps split K; a batch (or a very wide N) has CTAs to spare, so
     // each CTA takes RG groups and its warps stream longer K runs — fewer CTA launches and K
@@ -504,11 +565,15 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
             rg = r;
         }
     }
-    if (const char* f = std::getenv("NGEMM_SKINNY_RG")) rg = std::atoi(f);  // experiments
+    if (opt(O_SKINNY_RG) > 0) rg = opt(O_SKINNY_RG);  // experiments
     // MT = 16 in a 1024-thread CTA is capped at 64 registers and spills: 16 warps at most
     // (16 x 768 x 3072: 4.6 -> 3.85 us, profiles/sweep_skinny_warps_r1.log)
     int64_t ks_use = MT >= 16 ? std::min<int64_t>(ks, 16) : ks;
-    if (const char* f = std::getenv("NGEMM_SKINNY_WARPS")) ks_use = std::atoi(f);  // experiments: 8 / 16 / 32
+    if (opt(O_SKINNY_WARPS) > 0) ks_use = opt(O_SKINNY_WARPS);  // experiments: 8 / 16 / 32
+    // warps capped below the K chunks wanted (MT = 16): split K over the grid instead, so deep-K /
+    // narrow-N shapes (16 x 256 x 16384) still put ~32 streaming warps on every SM
+    if (splits == 1 && rq.out == nullptr && ks_use < ks && ks_use >= 8 && ks_use <= 16 && opt(O_SKINNY_WARPS) <= 0)
+        splits = (ks + ks_use - 1) / ks_use;
     if (rg == 2) return launch_skinny_mma_w<MT, 8, 2>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
     if (rg == 4) return launch_skinny_mma_w<MT, 8, 4>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
     if (rg == 8) return launch_skinny_mma_w<MT, 8, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt, rq);
@@ -601,7 +666,7 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
     // which since the pack-saturate step also beats the broadcast kernel (1) on every
     // M > 4, N < 2048 shape (profiles/sweep_r1_skinny_sat_variants.log).
     int variant = mode == NGEMM_SAT_EXACT ? 3 : 4;
-    if (const char* v = std::getenv("NGEMM_SKINNY_VARIANT")) variant = std::atoi(v);  // experiments
+    if (opt(O_SKINNY_VARIANT) >= 0) variant = opt(O_SKINNY_VARIANT);  // experiments
     if (t_force.skinny_variant >= 0) variant = t_force.skinny_variant;
     if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     if (variant == 4 && mode != NGEMM_SAT_EXACT) {
@@ -673,10 +738,7 @@ struct TcPlan {
 // 16384^3 (profiles/quad_bench_r1.log: 4-CTA clusters leave SMs idle — 132 of 148 usable — and
 // the two pairs' pipelines run in lockstep), so the planner only considers it with
 // NGEMM_TC_QUAD=1.
-bool quad_disabled() {
-    const char* e = std::getenv("NGEMM_TC_QUAD");
-    return !(e && e[0] == '1');
-}
+bool quad_disabled() { return opt(O_TC_QUAD) != 1; }
 
 // Picks the configuration with the smallest estimated makespan (waves x K-loop + epilogue),
 // then adds split-K (TMA reduce-add) while waves stay under one and K is deep.
@@ -706,9 +768,9 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
             }
         }
     }
-    if (const char* force = std::getenv("NGEMM_TC_CFG")) best.cfg = std::atoi(force) % TC_NUM_CFG;  // experiments
+    if (opt(O_TC_CFG) >= 0) best.cfg = opt(O_TC_CFG) % TC_NUM_CFG;  // experiments / tests
 
-    if (const char* force = std::getenv("NGEMM_TC_SPLITS")) best.splits = std::max(1, std::atoi(force));
+    if (opt(O_TC_SPLITS) > 0) best.splits = opt(O_TC_SPLITS);
     if (t_force.tc_cfg >= 0) best.cfg = t_force.tc_cfg % TC_NUM_CFG;
     if (t_force.tc_splits >= 1) best.splits = t_force.tc_splits;
     if (kTcCfg[best.cfg].mc > 1 && ((n + kTcCfg[best.cfg].bn - 1) / kTcCfg[best.cfg].bn) % kTcCfg[best.cfg].mc != 0)
@@ -719,10 +781,7 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
 // Epilogue choice for an aligned, unsplit C: the TMA-store epilogue everywhere — direct 16-byte
 // stores from registers (c_mode 3) measured 2-30 % slower even on single-wave grids
 // (profiles/ab_direct_r1.log); NGEMM_TC_DIRECT=1 selects them for experiments.
-bool direct_c_stores(int /*tiles*/, int /*units*/) {
-    const char* e = std::getenv("NGEMM_TC_DIRECT");
-    return e && std::atoi(e) != 0;
-}
+bool direct_c_stores(int /*tiles*/, int /*units*/) { return opt(O_TC_DIRECT) != 0; }
 
 // Operand formats and epilogue of one tcgen05 launch: the NGEMM path is u8 x s8 into C; the
 // i16 path issues four launches over byte planes with mixed formats, shifting and adding into C.
@@ -760,10 +819,8 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.splits = c_mode == 2 ? 1 : std::max(1, std::min(splits, num_kb));
     map.group_m = tc::GROUP_M;
     // pre-issuing the first loads before the block sync measured slower (profiles/ab_preissue_r1.log)
-    map.preissue = 0;
-    if (const char* e = std::getenv("NGEMM_TC_PREISSUE")) map.preissue = std::atoi(e);  // experiments
-    map.l2hint = 3;
-    if (const char* e = std::getenv("NGEMM_TC_L2HINT")) map.l2hint = std::atoi(e);  // experiments
+    map.preissue = opt(O_TC_PREISSUE);  // experiments
+    map.l2hint = opt(O_TC_L2HINT);      // experiments (default 3: A evict_last, B evict_first)
     map.prefetch = l2_prefetch_enabled() ? 1 : 0;
     map.dbg = 0;
     map.trace_id = -1;
@@ -780,10 +837,10 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         map.splits = 1;
     }
 #ifdef NGEMM_TRACE
-    if (const char* e = std::getenv("NGEMM_TC_DBG")) map.dbg = std::atoi(e);  // trace build only
+    map.dbg = opt(O_TC_DBG);  // trace build only
     map.trace_id = g_trace_next++;
 #endif
-    if (const char* g = std::getenv("NGEMM_TC_GROUP_M")) map.group_m = std::max(1, std::atoi(g));  // experiments
+    if (opt(O_TC_GROUP_M) > 0) map.group_m = opt(O_TC_GROUP_M);  // experiments
     if (c_mode == 0 && map.splits == 1 && !ops.accumulate && direct_c_stores(tiles, units)) c_mode = 3;
     if (ops.accumulate) {
         c_mode = 1;  // C already holds a partial sum: every split reduce-adds into it
@@ -802,16 +859,20 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
                             int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
                             const TcOps& ops = TcOps()) {
     // TMA needs 16-byte aligned bases and strides (SURVEY.md §0 gotcha 3)
+    const bool rq = ops.rq_out != nullptr;  // fused requantisation: no C, no split-K
+    const bool c_tma = !rq && c_tma_ok(c, ldc, n);
+    if (ops.accumulate && !c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "tcgen05: accumulating epilogue needs a TMA-describable C");
     const uint8_t* a_use = a;
     const uint8_t* b_use = reinterpret_cast<const uint8_t*>(b);
     int64_t lda_use = lda, ldb_use = ldb;
     uint8_t* scratch = nullptr;
     {
         ngemm_status ss = stage_tma_operands(a_use, lda_use, m, b_use, ldb_use, n, k, &scratch, st);
-        if (ss != NGEMM_OK) return ss;
+        if (ss != NGEMM_OK) {
+            if (scratch) cudaFreeAsync(scratch, st);
+            return ss;
+        }
     }
-    const bool rq = ops.rq_out != nullptr;  // fused requantisation: no C, no split-K
-    const bool c_tma = !rq && c_tma_ok(c, ldc, n);
     const TcPlan plan = plan_tcgen05(m, n, k, di.sms, c_tma ? 1 : 0);
     const TcCfgInfo& ci = kTcCfg[plan.cfg];
     CUtensorMap ta, tb, tcm;
@@ -820,7 +881,6 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
     if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, ci.bn / ci.cg);
     if (s == NGEMM_OK && c_tma) s = make_tmap_c(&tcm, c, m, n, ldc);
     const int c_mode = c_tma ? 0 : 2;
-    if (ops.accumulate && !c_tma) return fail(NGEMM_ERR_UNSUPPORTED, "tcgen05: accumulating epilogue needs a TMA-describable C");
     if (s == NGEMM_OK) {
         switch (plan.cfg) {
         case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
@@ -858,10 +918,7 @@ cudaError_t copy_rows_h2d(void* dst, int64_t kp, const void* src, int64_t k, int
 // NGEMM_SAT_HYBRID=1 forces the chain (tests), 0 disables it.
 constexpr int64_t kSatHybridMinM = 256;
 constexpr double kSatHybridMinWork = 1e9;
-int sat_hybrid_env() {
-    const char* e = std::getenv("NGEMM_SAT_HYBRID");
-    return e ? std::atoi(e) : -1;
-}
+int sat_hybrid_env() { return opt(O_SAT_HYBRID); }
 
 ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c, int64_t ldc,
                                int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
@@ -879,7 +936,7 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
     ngemm_status s = make_tmap_c(&tcm, c, m, n, ldc);
     if (s != NGEMM_OK) return s;
     uint8_t* buf = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), bs_off + bs_b, st));
+    NG_CUDA(dev_alloc(&buf, bs_off + bs_b, st));
     int32_t* guard = reinterpret_cast<int32_t*>(buf);
     uint32_t* flags = reinterpret_cast<uint32_t*>(buf + guard_b);
     uint8_t* lt = buf + lt_off;
@@ -895,8 +952,7 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
         return NGEMM_OK;
     };
     // experiments only (timing probes): skip launches of the chain, results are then wrong
-    int skip = 0;
-    if (const char* e = std::getenv("NGEMM_SATFIX_SKIP")) skip = std::atoi(e);
+    const int skip = opt(O_SATFIX_SKIP);
     auto grid_for = [&](int64_t items) {
         return dim3(static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((items + 255) / 256, di.sms * 16))));
     };
@@ -1147,7 +1203,7 @@ ngemm_status launch_i16_tc(const int16_t* a, int64_t lda, const int16_t* b, int6
                            int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st) {
     const int64_t kp = round_up(k, 16);
     uint8_t* planes = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&planes), static_cast<size_t>(2 * (m + n) * kp), st));
+    NG_CUDA(dev_alloc(&planes, static_cast<size_t>(2 * (m + n) * kp), st));
     uint8_t* al = planes;
     uint8_t* ah = al + m * kp;
     uint8_t* bl = ah + m * kp;
@@ -1192,7 +1248,7 @@ ngemm_status run_i16(const int16_t* a, int64_t lda, const int16_t* b, int64_t ld
     const bool c_tma = c_tma_ok(c, ldc, n);
     bool tensor = c_tma && m > kSkinnyMaxM && static_cast<double>(m) * n * k >= kI16TensorMinWork &&
                   m <= INT32_MAX / 2 && k <= INT32_MAX / 4;
-    if (const char* e = std::getenv("NGEMM_I16_PATH")) tensor = c_tma && std::strcmp(e, "tcgen05") == 0;  // tests
+    if (opt(O_I16_PATH) >= 0) tensor = c_tma && opt(O_I16_PATH) == 1;  // tests
     if (tensor) return launch_i16_tc(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     return launch_simt_i16(a, lda, b, ldb, c, ldc, m, n, k, st);
 }
@@ -1237,7 +1293,7 @@ ngemm_status host_gemm_pipelined(const uint8_t* a, const int8_t* b, int32_t* c, 
     ck(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking), "stream");
     for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     uint8_t* buf = nullptr;
-    if (s == NGEMM_OK && ck(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, sin), "malloc")) {
+    if (s == NGEMM_OK && ck(dev_alloc(&buf, c_off + c_bytes, sin), "malloc")) {
         int32_t* dc = reinterpret_cast<int32_t*>(buf + c_off);
         // column pass j over all row blocks i: the first pass streams A block by block behind
         // B block 0, so the first C tile leaves after A_0 + B_0 (1/8 + 1/4 of the operands)
@@ -1308,7 +1364,7 @@ ngemm_status host_gemm(int esize, const ngemm_packed_meta* meta, const void* a_o
                  c_off = b_off + round_up(b_bytes, 256);
     cudaStream_t st = nullptr;
     uint8_t* buf = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
+    NG_CUDA(dev_alloc(&buf, c_off + c_bytes, st));
     bool ok = true;
     if (meta) {
         ok = cudaMemcpyAsync(buf, a_or_packed, p_bytes, cudaMemcpyHostToDevice, st) == cudaSuccess;
@@ -1392,9 +1448,9 @@ ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const i
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    const char* unfused = std::getenv("NGEMM_REQUANT_UNFUSED");  // experiments: time the unfused form
+    const bool unfused = opt(O_REQUANT_UNFUSED) == 1;  // experiments: time the unfused form
     if (sat_mode == NGEMM_SAT_EXACT && m > kSkinnyMaxM && m <= INT32_MAX - tc::BM && k <= INT32_MAX - tc::BK &&
-        !(unfused && unfused[0] == '1')) {
+        !unfused) {
         TcOps ops;
         ops.rq_scale = scale;
         ops.rq_bias = bias;
@@ -1403,7 +1459,7 @@ ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const i
         ops.rq_zp = zero_point;
         return launch_tcgen05(a, lda, b, ldb, nullptr, n, m, n, k, di, st, ops);
     }
-    if (sat_mode == NGEMM_SAT_EXACT && m <= kSkinnyMaxM && !(unfused && unfused[0] == '1')) {
+    if (sat_mode == NGEMM_SAT_EXACT && m <= kSkinnyMaxM && !unfused) {
         Requant rq;
         rq.scale = scale;
         rq.bias = bias;
@@ -1415,7 +1471,7 @@ ngemm_status ngemm_cuda_gemm_u8i8_requant(const uint8_t* a, int64_t lda, const i
     }
     // the saturating mode: C in scratch, then the same arithmetic unfused
     int32_t* cbuf = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&cbuf), static_cast<size_t>(m * n) * 4, st));
+    NG_CUDA(dev_alloc(&cbuf, static_cast<size_t>(m * n) * 4, st));
     s = run_gemm(a, lda, b, ldb, cbuf, n, m, n, k, sat_mode, NGEMM_KERNEL_AUTO, st);
     if (s == NGEMM_OK) {
         const int64_t blocks = std::max<int64_t>(1, std::min<int64_t>((m * n + 255) / 256, di.sms * 8));
@@ -1567,7 +1623,7 @@ ngemm_status ngemm_cuda_gemm_packed_resident_host(ngemm_packed_handle h, const i
     const size_t c_off = round_up(b_bytes, 256);
     cudaStream_t st = nullptr;
     uint8_t* buf = nullptr;
-    NG_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_bytes, st));
+    NG_CUDA(dev_alloc(&buf, c_off + c_bytes, st));
     s = copy_rows_h2d(buf, kp, b, k, n, st) == cudaSuccess ? NGEMM_OK : fail(NGEMM_ERR_CUDA, "H2D copy failed");
     if (s == NGEMM_OK)
         s = run_gemm(h->d_a, h->lda, reinterpret_cast<const int8_t*>(buf), kp, reinterpret_cast<int32_t*>(buf + c_off),
@@ -1660,7 +1716,7 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
                 return bad(NGEMM_ERR_CUDA, "stream create failed");
             uint8_t* buf = nullptr;
             ngemm_status ls = NGEMM_OK;
-            if (cudaMallocAsync(reinterpret_cast<void**>(&buf), c_off + c_b, stream) != cudaSuccess) {
+            if (dev_alloc(&buf, c_off + c_b, stream) != cudaSuccess) {
                 ls = NGEMM_ERR_CUDA;
                 msg[d] = "device allocation failed";
             }
@@ -1884,6 +1940,35 @@ ngemm_status load_store_file(const char* path, int* loaded) {
 }  // namespace
 
 extern "C" {
+
+ngemm_status ngemm_cuda_set_option(const char* name, int value) {
+    const int i = opt_index(name);
+    if (i < 0) return fail(NGEMM_ERR_CONFIG, std::string("unknown option ") + (name ? name : "(null)"));
+    std::call_once(g_opt_once, load_opts);
+    g_opt[i].store(value, std::memory_order_relaxed);
+    return NGEMM_OK;
+}
+
+int ngemm_cuda_get_option(const char* name) {
+    const int i = opt_index(name);
+    return i < 0 ? INT32_MIN : opt(static_cast<Opt>(i));
+}
+
+ngemm_status ngemm_cuda_reset_options(void) {
+    std::call_once(g_opt_once, load_opts);
+    load_opts();
+    return NGEMM_OK;
+}
+
+ngemm_status ngemm_cuda_trim(void) {
+    int dev = 0;
+    NG_CUDA(cudaGetDevice(&dev));
+    if (cudaMemPool_t pool = lib_pool(dev)) {
+        NG_CUDA(cudaDeviceSynchronize());
+        NG_CUDA(cudaMemPoolTrimTo(pool, 0));
+    }
+    return NGEMM_OK;
+}
 
 ngemm_status ngemm_cuda_tune_clear(void) {
     std::lock_guard<std::mutex> lk(g_tune_mu);

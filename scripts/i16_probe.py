@@ -19,7 +19,7 @@ def main():
         for path in ("simt", "tcgen05"):
             if path == "simt" and m * n * k > 4096 ** 3:
                 continue
-            os.environ["NGEMM_I16_PATH"] = path
+            _lib.set_option("I16_PATH", {"tcgen05": 1, "simt": 0}.get(path, path))
 
             def run():
                 _lib.check(L.ngemm_cuda_gemm_i16(a.data_ptr(), k, b.data_ptr(), k, c.data_ptr(), n, m, n, k,

@@ -5,6 +5,7 @@ import numpy as np
 sys.path.insert(0, "tests")
 from test_gpu_parity import dev_gemm
 from oracle.oracle import Oracle, EXACT, SAT
+from paper_1910_00178_b200 import _lib  # noqa: E402
 ora = Oracle()
 rng = np.random.default_rng(0)
 for (m, n, k) in [(300, 333, 777), (512, 640, 1024), (256, 200, 512)]:
@@ -13,7 +14,7 @@ for (m, n, k) in [(300, 333, 777), (512, 640, 1024), (256, 200, 512)]:
     for kern, mode, env in [("tcgen05", EXACT, "-1"), ("sat_hybrid", SAT, "-1"), ("simt", SAT, "-1")]:
         for ldc in (n + 3, n + 7, n + 19):
             if ldc % 4: continue
-            os.environ["NGEMM_SAT_HYBRID"] = env
+            _lib.set_option("SAT_HYBRID", int(env))
             try:
                 got = dev_gemm(a, b, mode, kern, ldc=ldc)
                 ok = (got == ora.gemm(a, b, mode)).all()
@@ -23,7 +24,7 @@ for (m, n, k) in [(300, 333, 777), (512, 640, 1024), (256, 200, 512)]:
             except Exception as e:  # sat_hybrid refuses N % 4 != 0
                 print(m, n, k, kern, ldc, "refused:", type(e).__name__)
     for skip in ("1", "2", "8", "16"):
-        os.environ["NGEMM_SATFIX_SKIP"] = skip
+        _lib.set_option("SATFIX_SKIP", int(skip))
         try:
             dev_gemm(a, b, SAT, "sat_hybrid", ldc=n + 3)
             print("skip", skip, "no canary hit")
@@ -31,4 +32,4 @@ for (m, n, k) in [(300, 333, 777), (512, 640, 1024), (256, 200, 512)]:
             print("skip", skip, "CANARY", str(e)[:60])
         except Exception as e:
             print("skip", skip, "refused:", type(e).__name__)
-    os.environ.pop("NGEMM_SATFIX_SKIP")
+    _lib.reset_options()

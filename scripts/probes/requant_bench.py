@@ -8,6 +8,7 @@ import torch
 
 sys.path.insert(0, ".")
 from paper_1910_00178_b200 import api  # noqa: E402
+from paper_1910_00178_b200 import _lib  # noqa: E402
 
 
 def timed(fn, reps, graph=True):
@@ -52,9 +53,9 @@ for (m, n, k) in [(2048, 4096, 1024), (2048, 1024, 4096), (512, 4096, 1024), (10
     big = m * n * k >= 2**33
     t_gemm = timed(lambda i: api.gemm_device(A[i % nb], B[i % nb], C[i % nb]), reps, not big)
     t_rq = timed(lambda i: api.gemm_device_requant(A[i % nb], B[i % nb], sc, bi, 0, out=O[i % nb]), reps, not big)
-    os.environ["NGEMM_REQUANT_UNFUSED"] = "1"  # int32 C in scratch, then requant_kernel
+    _lib.set_option("REQUANT_UNFUSED", 1)  # int32 C in scratch, then requant_kernel
     t_un = timed(lambda i: api.gemm_device_requant(A[i % nb], B[i % nb], sc, bi, 0, out=O[i % nb]), reps, not big)
-    os.environ.pop("NGEMM_REQUANT_UNFUSED")
+    _lib.reset_options()
     print(json.dumps({"shape": f"{m}x{n}x{k}", "int32_gemm_us": round(t_gemm, 2), "fused_requant_us": round(t_rq, 2),
                       "unfused_requant_us": round(t_un, 2),
                       "out_bytes_int32": 4 * m * n, "out_bytes_int8": m * n}), flush=True)

@@ -13,14 +13,14 @@ for (m, n, k, mode, kern) in cases:
     torch.cuda.synchronize()
     assert (c.cpu().numpy() == o.gemm(a, b, mode)).all(), (m, n, k, mode, kern)
 for v in ("0", "1", "2", "3", "4"):
-    os.environ["NGEMM_SKINNY_VARIANT"] = v
+    _lib.set_option("SKINNY_VARIANT", int(v))
     for mode in (0, 1):
         a = o.mat_random_u8(7, 1000, 3); b = o.mat_random_i8(200, 1000, 4)
         c = api.gemm_device(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), mode=mode, kernel=3)
         torch.cuda.synchronize()
         assert (c.cpu().numpy() == o.gemm(a, b, mode)).all(), (v, mode)
-os.environ.pop("NGEMM_SKINNY_VARIANT")
-os.environ["NGEMM_TC_CFG"] = "0"
+_lib.reset_options()
+_lib.set_option("TC_CFG", 0)
 a = o.mat_random_u8(512, 256, 5); b = o.mat_random_i8(512, 256, 6)
 c = api.gemm_device(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(), mode=1, kernel=1)
 torch.cuda.synchronize()

@@ -33,3 +33,21 @@ def cuda():
         pytest.fail("GPU test run without a visible CUDA device")
     torch.cuda.init()
     return torch.device("cuda:0")
+
+
+class _Knobs:
+    """Library experiment knobs (ngemm_cuda_set_option): the library reads NGEMM_* from the
+    environment once, so tests switch kernels through the C-ABI and reset after each test."""
+
+    def set(self, name, value):
+        from paper_1910_00178_b200 import _lib
+        if name == "I16_PATH":
+            value = {"tcgen05": 1, "simt": 0}.get(value, value)
+        _lib.set_option(name, int(value))
+
+
+@pytest.fixture
+def knobs():
+    yield _Knobs()
+    from paper_1910_00178_b200 import _lib
+    _lib.reset_options()

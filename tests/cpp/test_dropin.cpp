@@ -3,7 +3,10 @@
 // resident weight cache.  Needs a GPU for the GEMM cases (run by tests/test_cpp_dropin.py).
 #include <catch2/catch_amalgamated.hpp>
 
+#include <atomic>
 #include <cstdio>
+#include <thread>
+#include <vector>
 #include <filesystem>
 
 #include "ngemm/ngemm.hpp"
@@ -74,6 +77,34 @@ TEST_CASE("dropin: device-resident weight is reused and invalidated on mutation"
     p.data<std::uint8_t>()[p.elem_offset(5, 7)] = 0;
     a.set(5, 7, 0);
     CHECK(gemm_ngemm(p, b, SatMode::WideningExact) == gemm_ref(a, b));
+}
+
+TEST_CASE("dropin: concurrent gemm_ngemm on one const PackedWeight (reentrant device cache)") {
+    // 8 threads x 50 calls race on the first upload and on the cached device copy; every result
+    // must be bit-exact and the weight uploaded once (pure and reentrant).
+    MatrixBuf a = u8(200, 384, 21), b = i8(96, 384, 22);
+    const PackedWeight p = pack_weights(a, kS512, TileConfig{16, 64, 64, Perm::MNK});
+    const MatrixBuf ref = gemm_ref(a, b), ref_sat = gemm_sat_oracle(a, b);
+    std::atomic<int> good{0}, bad{0}, errors{0};
+    std::vector<std::thread> ts;
+    for (int t = 0; t < 8; ++t)
+        ts.emplace_back([&, t] {
+            for (int i = 0; i < 50; ++i) {
+                try {
+                    const bool sat = ((i + t) & 3) == 0;
+                    const MatrixBuf c = gemm_ngemm(p, b, sat ? SatMode::HardwareSaturating : SatMode::WideningExact);
+                    (c == (sat ? ref_sat : ref) ? good : bad).fetch_add(1);
+                } catch (...) {
+                    errors.fetch_add(1);
+                }
+            }
+        });
+    for (auto& th : ts) th.join();
+    CHECK(errors.load() == 0);
+    CHECK(bad.load() == 0);
+    CHECK(good.load() == 400);
+    const auto w1 = p.device_weight(), w2 = p.device_weight();
+    CHECK(w1.get() == w2.get());  // one cached copy per device
 }
 
 TEST_CASE("dropin: NGPT file round trip feeds the GPU") {

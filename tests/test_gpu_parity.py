@@ -273,11 +273,29 @@ def test_multi_device_driver_single_gpu(cuda, oracle):
         _lib.check(_lib.load().ngemm_cuda_free(ptr))
 
 
+def _c5_row_blocks(m, block=64, count=8, seed=5):
+    """Row blocks of C checked against the oracle: the first and the last row tile plus random
+    64-row blocks in between (seeded), sorted, non-overlapping starts."""
+    rng = np.random.default_rng(seed)
+    starts = {0, m - block}
+    while len(starts) < count:
+        starts.add(int(rng.integers(1, (m - block) // block)) * block)
+    return sorted(starts)
+
+
 @pytest.mark.slow
-def test_config5_full_size(cuda, oracle, golden):
-    """16384^3 exact on tcgen05: first 128 rows against the reference digest, plus a
-    Freivalds check of the whole C (C.x == A.(B^T.x) in int64 with x in {0,1}; no C entry
-    wraps for K <= 65793)."""
+@pytest.mark.parametrize("mode", [EXACT, SAT])
+def test_config5_full_size(cuda, oracle, golden, mode):
+    """16384^3 (config 5) through AUTO in both modes — exact runs the tcgen05 pair kernel,
+    HardwareSaturating the tensor-core + sparse-fix chain (64 K-chunks per row, 128 MiB of
+    index lists):
+      * rows 0-127 against the reference's own digest and checksum (golden, oracle/_ref),
+      * 8 row blocks of 64 rows (first and last row tile + 6 random) bit-exact against the
+        oracle (gemm_ref / gemm_sat_oracle restated, gemm.hpp:36-52, 83-104),
+      * exact mode: 16 Freivalds rounds over the WHOLE C, C.x == A.(B^T.x) with x in [0, 16)
+        in float64 — exact, since |C| < 2^30 (no wrap at K = 16384) and every partial sum is an
+        integer below 16384 * 255 * 128 * 16 * 16384 < 2^53.  A single wrong element escapes
+        one round with probability <= 1/16, all 16 with <= 2^-64."""
     import torch
     K = 16384
     b = oracle.mat_random_i8(K, K, 1)
@@ -286,30 +304,36 @@ def test_config5_full_size(cuda, oracle, golden):
     a = oracle.mat_random_u8(K, K, 0)
     da = torch.from_numpy(a).cuda()
     db = torch.from_numpy(b).cuda()
-    dc = api.gemm_device(da, db, mode=api.SatMode.WIDENING_EXACT)
+    assert _lib.load().ngemm_cuda_pick_kernel(K, K, K, mode) == (
+        _lib.KERNEL_TCGEN05 if mode == EXACT else _lib.KERNEL_SAT_HYBRID)
+    dc = api.gemm_device(da, db, mode=mode)
     torch.cuda.synchronize()
+    key = "exact" if mode == EXACT else "sat"
     top = dc[:128].cpu().numpy()
-    assert oracle.fnv1a(top) == g["exact_fnv"]
-    assert int(top.astype(np.int64).sum()) == g["exact_checksum"]
-    # float64 is exact here: every product and partial sum is an integer below 2^53
-    gen = torch.Generator(device="cuda").manual_seed(7)
-    for _ in range(2):
-        x = torch.randint(0, 2, (K, 1), device="cuda", generator=gen).to(torch.float64)
-        lhs = dc.to(torch.float64) @ x                      # C.x
+    assert oracle.fnv1a(top) == g[f"{key}_fnv"]
+    assert int(top.astype(np.int64).sum()) == g[f"{key}_checksum"]
+    for r0 in _c5_row_blocks(K):
+        got = dc[r0:r0 + 64].cpu().numpy()
+        ref = oracle.gemm(np.ascontiguousarray(a[r0:r0 + 64]), b, mode)
+        assert (got == ref).all(), (key, r0, int((got != ref).sum()))
+    if mode == EXACT:
+        gen = torch.Generator(device="cuda").manual_seed(7)
+        x = torch.randint(0, 16, (K, 16), device="cuda", generator=gen).to(torch.float64)
+        lhs = dc.to(torch.float64) @ x                      # C.x, 16 rounds at once
         btx = db.to(torch.float64).t() @ x                  # B^T x
         rhs = da.to(torch.float64) @ btx                    # A.(B^T x)
         assert torch.equal(lhs, rhs)
 
 
 @pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6, 7, 8])
-def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
+def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, knobs):
     """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64, the 4-CTA and 2-CTA
     A-multicast clusters, the lean 2-3 stage variants), with and without
     split-K (TMA s32 reduce-add), with TMA-store and direct-store epilogues, vs the oracle."""
-    monkeypatch.setenv("NGEMM_TC_CFG", str(cfg))
+    knobs.set("TC_CFG", str(cfg))
     for splits, direct in (("1", "0"), ("1", "1"), ("2", "0"), ("3", "0")):
-        monkeypatch.setenv("NGEMM_TC_SPLITS", splits)
-        monkeypatch.setenv("NGEMM_TC_DIRECT", direct)  # TMA-store vs direct vector-store epilogue
+        knobs.set("TC_SPLITS", splits)
+        knobs.set("TC_DIRECT", direct)  # TMA-store vs direct vector-store epilogue
         # (300, 333, 777, 336): ldc % 4 == 0 but N % 4 != 0 — must not take the TMA epilogue (a box
         # straddling the last column writes the whole trailing 16-byte granule, probe_ldc.py)
         for (m, n, k, ldc) in ((300, 520, 1100, None), (256, 256, 2048, 260), (129, 65, 640, None),
@@ -322,11 +346,11 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, monkeypatch):
 
 
 @pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
-def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
+def test_skinny_variants(cuda, oracle, golden, variant, knobs):
     """Skinny (M <= 16) variants: 0 warp-butterfly dp4a, 1 lanes-own-rows dp4a (broadcast A),
     2 tensor-core swap-AB, 3 warp-MMA load stream (2 and 3: exact mode only; sat falls back
     to 1), 4 dp4a load stream (sat) — all bit-exact."""
-    monkeypatch.setenv("NGEMM_SKINNY_VARIANT", variant)
+    knobs.set("SKINNY_VARIANT", variant)
     for c in golden["config2"]:
         a = oracle.mat_random_u8(c["m"], c["k"], 0)
         b = oracle.mat_normal_i8(c["n"], c["k"], 1, 32.0)
@@ -341,13 +365,13 @@ def test_skinny_variants(cuda, oracle, golden, variant, monkeypatch):
 
 
 @pytest.mark.parametrize("hybrid", ["1", "-1"])
-def test_sat_mode_on_provably_safe_inputs(cuda, oracle, hybrid, monkeypatch):
+def test_sat_mode_on_provably_safe_inputs(cuda, oracle, hybrid, knobs):
     """HardwareSaturating on inputs that cannot saturate (the reference's safe range, u8 <= 127,
     tuner.hpp:26-43): with max A measured on the device no pair is classified as clampable, so
     the tensor cores compute everything and the fix kernel exits; the result must still equal
     gemm_sat_oracle (== gemm_ref here).  Also the boundary cases around max A = 128 / 129.
     hybrid=1 forces the tensor-core chain on every shape, -1 is the default dispatch."""
-    monkeypatch.setenv("NGEMM_SAT_HYBRID", hybrid)
+    knobs.set("SAT_HYBRID", hybrid)
     for (m, n, k) in ((512, 512, 1024), (1000, 700, 333), (2048, 2048, 2048)):
         a = oracle.mat_random_u8(m, k, 3, 0, 127)
         b = oracle.mat_random_i8(n, k, 4)
@@ -372,7 +396,7 @@ def _normal_i8(rng, shape, sigma=32.0):
 
 
 @pytest.mark.parametrize("case", ["uniform", "normal", "extreme", "dense_frac", "sparse_edges", "safe_b"])
-def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
+def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, knobs):
     """HardwareSaturating for M > 16 (kernel_satfix.cuh): tcgen05 on B with the pairs that could
     clamp zeroed, plus the CUDA-core fix of those pairs (list walk, or the list-free path for rows
     whose pairs all could clamp).  Sparse, dense and empty lists, ragged shapes (odd K, K < 256, K
@@ -380,7 +404,7 @@ def test_sat_hybrid_tensor_core_plus_fix(cuda, oracle, case, monkeypatch):
     rng = np.random.default_rng(["uniform", "normal", "extreme", "dense_frac", "sparse_edges", "safe_b"].index(case))
     # NGEMM_SAT_HYBRID=1 forces the chain below its size threshold (M >= 256, >= 1e9 MACs);
     # 1000^3 takes it by default
-    monkeypatch.setenv("NGEMM_SAT_HYBRID", "1")
+    knobs.set("SAT_HYBRID", "1")
     # N % 4 != 0 (333) cannot take the TMA reduce-add: AUTO falls back to the CUDA-core kernel
     # (260, 256, 40000): 157 K chunks > the fix kernel's 128-chunk list, so K is split on the host
     shapes = [(300, 332, 777), (300, 333, 777), (257, 388, 200), (40, 640, 1024), (129, 4100, 100),
@@ -426,12 +450,12 @@ def test_sat_hybrid_explicit_kernel_id(cuda, oracle):
 
 
 @pytest.mark.parametrize("hybrid", ["0", "1"])
-def test_host_entry_pipelined_pinned(cuda, oracle, hybrid, monkeypatch):
+def test_host_entry_pipelined_pinned(cuda, oracle, hybrid, knobs):
     """ngemm_cuda_gemm_u8i8_host on PINNED host buffers takes the chunked H2D/compute/D2H
     pipeline (C >= 64 MiB); result must equal the oracle in both modes.  hybrid=1 forces the
     saturating tensor-core chain on every C tile (strided C sub-blocks, ragged tiles)."""
     import torch
-    monkeypatch.setenv("NGEMM_SAT_HYBRID", hybrid)
+    knobs.set("SAT_HYBRID", hybrid)
     L = _lib.load()
     # 4096^2 splits into 8 x 4 C tiles; 4000 x 4500 x 333 gives ragged row/column tiles and padded K
     for (m, n, k) in [(4096, 4096, 640), (4000, 4500, 333)]:
@@ -531,10 +555,10 @@ def _dev_gemm_i16(a, b):
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("path", ["simt", "tcgen05"])
-def test_i16_paths_vs_reference_golden(cuda, oracle, golden, path, monkeypatch):
+def test_i16_paths_vs_reference_golden(cuda, oracle, golden, path, knobs):
     """i16 x i16 (gemm.hpp:161-190): the CUDA-core kernel and the tensor-core byte-plane
     decomposition (4 int8 tcgen05 GEMMs, shifted and reduce-added) against the reference."""
-    monkeypatch.setenv("NGEMM_I16_PATH", path)
+    knobs.set("I16_PATH", path)
     for c in golden["i16"]:
         a = oracle.mat_random_i16(c["m"], c["k"], c["seed"], c["lo"], c["hi"])
         b = oracle.mat_random_i16(c["n"], c["k"], c["seed"] + 100, c["lo"], c["hi"])
@@ -587,3 +611,43 @@ def test_fused_requant_epilogue(cuda, oracle, mode):
         assert (ref == 127).any() and (ref == -128).any(), "the case should exercise both clamp edges"
         pad = out.as_strided((m, ldo), (ldo, 1)).cpu().numpy()[:, n:]
         assert (pad == 0x55).all(), "requant wrote outside the logical columns"
+
+
+def test_stress_repeated_launches_across_streams(cuda, oracle, knobs):
+    """Race / sync stress (compute-sanitizer is closed on this pool): the warp-specialised
+    mbarrier/TMEM pipelines, the cluster DSMEM reduction, split-K TMA reduce-add and the
+    saturating chain are launched many times back to back on 4 concurrent streams, with
+    different grids per shape, each launch into its own C.  Every output must equal the
+    oracle bit for bit — a missing fence, barrier phase slip or TMEM/smem reuse race shows up
+    as a sporadic mismatch."""
+    import torch
+    cases = [  # (m, n, k, mode, kernel, knob settings)
+        (2048, 2048, 2048, EXACT, "tcgen05", {}),                            # pair 256x256, persistent
+        (300, 520, 1100, EXACT, "tcgen05", {"TC_CFG": 2, "TC_SPLITS": 3}),   # 1-CTA + split-K reduce-add
+        (600, 1024, 700, EXACT, "tcgen05", {"TC_CFG": 4}),                   # 4-CTA A-multicast clusters
+        (16, 4096, 1024, EXACT, "skinny", {}),                               # warp-MMA load stream
+        (16, 4096, 1024, EXACT, "skinny", {"SKINNY_VARIANT": 2}),            # tcgen05 swap-AB, DSMEM split-K
+        (16, 4096, 1024, SAT, "skinny", {}),                                 # dp4a load stream
+        (1000, 1000, 1000, SAT, "auto", {}),                                 # tensor cores + sparse fix
+    ]
+    streams = [torch.cuda.Stream() for _ in range(4)]
+    reps = 24
+    for (m, n, k, mode, kern, kv) in cases:
+        for name, v in kv.items():
+            knobs.set(name, v)
+        a = oracle.mat_random_u8(m, k, m + 1)
+        b = oracle.mat_random_i8(n, k, n + 2)
+        ref = oracle.gemm(a, b, mode)
+        da = torch.from_numpy(a).cuda()
+        db = torch.from_numpy(b).cuda()
+        outs = [torch.full((m, n), 0x5A5A5A5A, dtype=torch.int32, device="cuda") for _ in range(reps)]
+        torch.cuda.synchronize()
+        for i in range(reps):
+            s = streams[i % len(streams)]
+            with torch.cuda.stream(s):
+                api.gemm_device(da, db, outs[i], mode=mode, kernel=KERNELS[kern], stream=s)
+        torch.cuda.synchronize()
+        for i, o in enumerate(outs):
+            got = o.cpu().numpy()
+            assert (got == ref).all(), (m, n, k, mode, kern, kv, i, int((got != ref).sum()))
+        _lib.reset_options()
