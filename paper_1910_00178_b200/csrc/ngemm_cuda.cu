@@ -1262,89 +1262,11 @@ bool is_pinned(const void* p) {
     return attr.type == cudaMemoryTypeHost;
 }
 
-// Large GEMM on PINNED host buffers, pipelined over a ti x tj grid of C tiles (column passes):
-// A's row blocks and B's row blocks (= C's column blocks) stream in on a copy-in stream in
-// first-use order,
-// each tile's GEMM runs on a compute stream as soon as its A and B blocks have landed, and its C
-// tile goes back on a copy-out stream (a pitched D2H into the row-major host C).  H2D, tensor-
-// core compute and D2H overlap (PCIe is full duplex); tiling B as well as A lets the first C
-// bytes leave after 1/ti + 1/tj of the operands have arrived instead of after all of B, so the
-// end-to-end time approaches the D2H of C alone.
-ngemm_status host_gemm_pipelined(const uint8_t* a, const int8_t* b, int32_t* c, int64_t m, int64_t n, int64_t k,
-                                 int sat_mode, int kernel) {
-    const int64_t kp = round_up(k, 16);
-    const int ti_want = 8, tj_want = n >= 4096 ? 4 : 1;
-    const int64_t rchunk = round_up((m + ti_want - 1) / ti_want, 256);
-    const int64_t cchunk = round_up((n + tj_want - 1) / tj_want, 256);
-    const int ti = static_cast<int>((m + rchunk - 1) / rchunk), tj = static_cast<int>((n + cchunk - 1) / cchunk);
-    const size_t a_bytes = static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
-    const size_t c_bytes = static_cast<size_t>(m * n) * 4;
-    const size_t b_off = round_up(static_cast<int64_t>(a_bytes), 256), c_off = b_off + round_up(b_bytes, 256);
-    cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
-    // events: A blocks [0, ti), B blocks [ti, ti + tj), C tiles after, one "done"
-    std::vector<cudaEvent_t> ev(static_cast<size_t>(ti + tj + ti * tj + 1), nullptr);
-    ngemm_status s = NGEMM_OK;
-    auto ck = [&](cudaError_t e, const char* what) {
-        if (e != cudaSuccess && s == NGEMM_OK) s = fail(NGEMM_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
-        return s == NGEMM_OK;
-    };
-    ck(cudaStreamCreateWithFlags(&sin, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&scomp, cudaStreamNonBlocking), "stream");
-    ck(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking), "stream");
-    for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
-    uint8_t* buf = nullptr;
-    if (s == NGEMM_OK && ck(dev_alloc(&buf, c_off + c_bytes, sin), "malloc")) {
-        int32_t* dc = reinterpret_cast<int32_t*>(buf + c_off);
-        // column pass j over all row blocks i: the first pass streams A block by block behind
-        // B block 0, so the first C tile leaves after A_0 + B_0 (1/8 + 1/4 of the operands)
-        // and the copy-in keeps pace with the copy-out; later passes only add one B block.
-        for (int j = 0; j < tj && s == NGEMM_OK; ++j) {
-            const int64_t c0 = j * cchunk, cols = std::min(cchunk, n - c0);
-            for (int i = 0; i < ti && s == NGEMM_OK; ++i) {
-                const int64_t r0 = i * rchunk, rows = std::min(rchunk, m - r0);
-                if (j == 0) {
-                    if (i == 0) {
-                        ck(copy_rows_h2d(buf + b_off, kp, b, k, cols, sin), "H2D B");
-                        ck(cudaEventRecord(ev[ti], sin), "record");
-                    }
-                    ck(copy_rows_h2d(buf + r0 * kp, kp, a + r0 * k, k, rows, sin), "H2D A");
-                    ck(cudaEventRecord(ev[i], sin), "record");
-                } else if (i == 0) {
-                    ck(copy_rows_h2d(buf + b_off + c0 * kp, kp, b + c0 * k, k, cols, sin), "H2D B");
-                    ck(cudaEventRecord(ev[ti + j], sin), "record");
-                }
-                ck(cudaStreamWaitEvent(scomp, ev[i], 0), "wait");
-                ck(cudaStreamWaitEvent(scomp, ev[ti + j], 0), "wait");
-                if (s == NGEMM_OK)
-                    s = run_gemm(buf + r0 * kp, kp, reinterpret_cast<const int8_t*>(buf + b_off + c0 * kp), kp,
-                                 dc + r0 * n + c0, n, rows, cols, k, sat_mode, kernel, scomp);
-                cudaEvent_t ev_c = ev[ti + tj + i * tj + j];
-                ck(cudaEventRecord(ev_c, scomp), "record");
-                ck(cudaStreamWaitEvent(sout, ev_c, 0), "wait");
-                if (tj == 1)
-                    ck(cudaMemcpyAsync(c + r0 * n, dc + r0 * n, static_cast<size_t>(rows * n) * 4,
-                                       cudaMemcpyDeviceToHost, sout), "D2H C");
-                else
-                    ck(cudaMemcpy2DAsync(c + r0 * n + c0, static_cast<size_t>(n) * 4, dc + r0 * n + c0,
-                                         static_cast<size_t>(n) * 4, static_cast<size_t>(cols) * 4,
-                                         static_cast<size_t>(rows), cudaMemcpyDeviceToHost, sout), "D2H C");
-            }
-        }
-        cudaEvent_t ev_done = ev.back();
-        ck(cudaEventRecord(ev_done, sout), "record");
-        cudaStreamWaitEvent(sin, ev_done, 0);
-        cudaFreeAsync(buf, sin);
-    }
-    if (sin) ck(cudaStreamSynchronize(sin), "sync");
-    if (sout) ck(cudaStreamSynchronize(sout), "sync");
-    if (scomp) ck(cudaStreamSynchronize(scomp), "sync");
-    for (auto& e : ev)
-        if (e) cudaEventDestroy(e);
-    if (sin) cudaStreamDestroy(sin);
-    if (scomp) cudaStreamDestroy(scomp);
-    if (sout) cudaStreamDestroy(sout);
-    return s;
-}
+}  // namespace
+
+#include "host_pipeline.cuh"
+
+namespace {
 
 // Host operands -> pooled device buffers (rows padded to 16 bytes for TMA) -> optional device
 // repack of a packed weight -> GEMM -> host C.  esize selects the u8 x i8 or i16 x i16 path.
@@ -1362,7 +1284,7 @@ ngemm_status host_gemm(int esize, const ngemm_packed_meta* meta, const void* a_o
     const size_t c_bytes = static_cast<size_t>(m * n) * 4;
     const size_t a_off = round_up(static_cast<int64_t>(p_bytes), 256), b_off = a_off + round_up(a_bytes, 256),
                  c_off = b_off + round_up(b_bytes, 256);
-    cudaStream_t st = nullptr;
+    cudaStream_t st = cudaStreamPerThread;
     uint8_t* buf = nullptr;
     NG_CUDA(dev_alloc(&buf, c_off + c_bytes, st));
     bool ok = true;
@@ -1601,9 +1523,24 @@ ngemm_status ngemm_cuda_gemm_u8i8_host(const uint8_t* a, const int8_t* b, int32_
     DevInfo di;
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
-    // big outputs on pinned host memory: overlap H2D / compute / D2H in row chunks
-    if (m >= 1024 && static_cast<double>(m) * n * 4 >= 64.0 * (1 << 20) && is_pinned(a) && is_pinned(c))
-        return host_gemm_pipelined(a, b, c, m, n, k, sat_mode, kernel);
+    // big problems: overlap H2D / compute / D2H over a grid of C tiles (pageable operands move
+    // through pinned staging slots)
+    if (pipeline_worth(m, n, k)) {
+        HostGemm g;
+        g.a_host = a;
+        g.b_host = b;
+        g.c_host = c;
+        g.a_pinned = is_pinned(a);
+        g.b_pinned = is_pinned(b);
+        g.c_pinned = is_pinned(c);
+        g.m = m;
+        g.n = n;
+        g.k = k;
+        g.mode = sat_mode;
+        g.kernel = kernel;
+        s = host_pipeline(g);
+        if (s != NGEMM_ERR_UNSUPPORTED) return s;
+    }
     return host_gemm(1, nullptr, a, 0, b, c, m, n, k, sat_mode, kernel);
 }
 
@@ -1618,10 +1555,26 @@ ngemm_status ngemm_cuda_gemm_packed_resident_host(ngemm_packed_handle h, const i
     s = current_device(&dev, &di);
     if (s != NGEMM_OK) return s;
     if (dev != h->device) return fail(NGEMM_ERR_UNSUPPORTED, "weight handle lives on another device");
+    if (pipeline_worth(h->m, n, h->k)) {  // B streams in by column blocks, C tiles stream out
+        HostGemm g;
+        g.a_dev = h->d_a;
+        g.lda_dev = h->lda;
+        g.b_host = b;
+        g.c_host = c;
+        g.b_pinned = is_pinned(b);
+        g.c_pinned = is_pinned(c);
+        g.m = h->m;
+        g.n = n;
+        g.k = h->k;
+        g.mode = sat_mode;
+        g.kernel = NGEMM_KERNEL_AUTO;
+        s = host_pipeline(g);
+        if (s != NGEMM_ERR_UNSUPPORTED) return s;
+    }
     const int64_t k = h->k, m = h->m, kp = round_up(k, 16);
     const size_t b_bytes = static_cast<size_t>(n * kp), c_bytes = static_cast<size_t>(m * n) * 4;
     const size_t c_off = round_up(b_bytes, 256);
-    cudaStream_t st = nullptr;
+    cudaStream_t st = cudaStreamPerThread;
     uint8_t* buf = nullptr;
     NG_CUDA(dev_alloc(&buf, c_off + c_bytes, st));
     s = copy_rows_h2d(buf, kp, b, k, n, st) == cudaSuccess ? NGEMM_OK : fail(NGEMM_ERR_CUDA, "H2D copy failed");

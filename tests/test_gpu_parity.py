@@ -470,6 +470,60 @@ def test_host_entry_pipelined_pinned(cuda, oracle, hybrid, knobs):
             assert (tc.numpy() == oracle.gemm(a, b, mode)).all(), (m, n, k, mode)
 
 
+@pytest.mark.parametrize("pinning", ["none", "a_only", "c_only"])
+def test_host_entry_pipelined_pageable_staging(cuda, oracle, pinning):
+    """The host pipeline on PAGEABLE buffers (what gemm_conventional on std::vector-backed
+    MatrixBufs passes): operands and C move through the pinned staging ring, copied by the host
+    worker pool; mixed pinned / pageable operands take the direct copy for the pinned ones.
+    Ragged tiles, K not a multiple of 16, growing row blocks, a C tile wider than one slot."""
+    import torch
+    L = _lib.load()
+    for (m, n, k) in [(4000, 4500, 333), (2304, 4000, 4100), (6000, 2048, 64)]:
+        a = oracle.mat_random_u8(m, k, 21)
+        b = oracle.mat_random_i8(n, k, 22)
+        c = np.full((m, n), -1, np.int32)
+        if pinning == "a_only":
+            ta = torch.from_numpy(a).pin_memory()
+            a_ptr, b_ptr, c_ptr, out = ta.data_ptr(), b.ctypes.data, c.ctypes.data, c
+        elif pinning == "c_only":
+            tc = torch.from_numpy(c).pin_memory()
+            a_ptr, b_ptr, c_ptr, out = a.ctypes.data, b.ctypes.data, tc.data_ptr(), None
+        else:
+            a_ptr, b_ptr, c_ptr, out = a.ctypes.data, b.ctypes.data, c.ctypes.data, c
+        for mode in (EXACT, SAT):
+            _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_ptr, b_ptr, c_ptr, m, n, k, mode, 0))
+            got = out if out is not None else tc.numpy()
+            assert (got == oracle.gemm(a, b, mode)).all(), (pinning, m, n, k, mode)
+
+
+@pytest.mark.parametrize("pinned", [True, False])
+def test_resident_weight_host_pipeline(cuda, oracle, pinned):
+    """gemm_ngemm's path: the weight A resident in HBM (packed handle), B streamed in by column
+    blocks and C tiles streamed out (ngemm_cuda_gemm_packed_resident_host), pinned or pageable."""
+    import ctypes as C
+    import torch
+    L = _lib.load()
+    for (m, n, k) in [(3000, 5000, 777), (1024, 8192, 128)]:
+        a = oracle.mat_random_u8(m, k, 31)
+        b = oracle.mat_random_i8(n, k, 32)
+        da = torch.from_numpy(a).cuda()
+        h = C.c_void_p()
+        _lib.check(L.ngemm_cuda_packed_from_device(da.data_ptr(), k, m, k, C.byref(h)))
+        try:
+            for mode in (EXACT, SAT):
+                if pinned:
+                    tb = torch.from_numpy(b).pin_memory()
+                    tc = torch.full((m, n), -1, dtype=torch.int32).pin_memory()
+                    _lib.check(L.ngemm_cuda_gemm_packed_resident_host(h, tb.data_ptr(), tc.data_ptr(), n, mode))
+                    got = tc.numpy()
+                else:
+                    got = np.full((m, n), -1, np.int32)
+                    _lib.check(L.ngemm_cuda_gemm_packed_resident_host(h, b.ctypes.data, got.ctypes.data, n, mode))
+                assert (got == oracle.gemm(a, b, mode)).all(), (pinned, m, n, k, mode)
+        finally:
+            L.ngemm_cuda_packed_free(h)
+
+
 def test_autotuner_picks_verified_config_and_dispatch_stays_exact(cuda, oracle, tmp_path):
     """GPU autotuner (tuner.hpp:132-175 re-targeted): the record names a configuration that was
     verified against the reference kernel; afterwards the dispatcher uses it and results stay
