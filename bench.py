@@ -564,6 +564,15 @@ def run_ours(args):
     torch.cuda.synchronize()
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
+    per_rank = None
+    if world > 1:  # every rank's own device time per step and its rows (load balance of the M shard)
+        import torch.distributed as dist
+        t = torch.tensor([ms_local / steps, float(mr)], dtype=torch.float64, device=dev)
+        allt = torch.empty((world, 2), dtype=torch.float64, device=dev)
+        dist.all_gather_into_tensor(allt, t)
+        per_rank = [{"rank": r, "rows": int(allt[r, 1].item()), "ms_per_step": round(float(allt[r, 0].item()), 4),
+                     "TOPS": round(2.0 * float(allt[r, 1].item()) * N * K / (float(allt[r, 0].item()) * 1e-3) / 1e12, 1)
+                     if allt[r, 0].item() > 0 else None} for r in range(world)]
     ms_step = ms / steps
     total_ops = 2.0 * M * N * K
     value = total_ops / (ms_step * 1e-3) / 1e12  # TOPS, whole job
@@ -663,6 +672,8 @@ def run_ours(args):
         if shapes is not None:
             line["shapes"] = shapes
             line["shapes_verified"] = all(s.get("verified") is True for s in shapes)
+        if per_rank is not None:
+            line["per_rank"] = per_rank
         if gather is not None:
             line["gather"] = gather
         print(json.dumps(line), flush=True)

@@ -177,6 +177,22 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
                                         int32_t* c, int64_t m, int64_t n, int64_t k, int sat_mode,
                                         int gather_device, int32_t** gathered);
 ngemm_status ngemm_cuda_free(void* device_ptr);
+/* The multi-GPU driver enables peer access between the listed devices, copies B over PCIe ONCE
+ * (into devices[0]) and relays it device to device over NVLink in 16 MiB chunks; each device
+ * then streams its A rows in and its C rows out through the host pipeline (pinned or pageable
+ * host buffers), and with a gather also peer-copies its C rows into the gather buffer. */
+
+/* Sharded resident weight (gemm_ngemm over several GPUs, layout.hpp:159-161): the packed rows
+ * are split into tile-aligned blocks of whole tm-strips (ngemm_cuda_shard_rows, align =
+ * lcm(tm, 128)); out[d] receives the handle of device devices[d] (NULL when that device gets no
+ * rows).  Free each with ngemm_cuda_packed_free.  u8 weights. */
+ngemm_status ngemm_cuda_packed_upload_sharded(const ngemm_packed_meta* meta, const uint8_t* host_packed,
+                                              size_t nbytes, const int* devices, int ndev,
+                                              ngemm_packed_handle* out /* ndev */);
+/* C[M x N] (host) = the sharded weight x B^T: B replicated by one H2D + NVLink relay, each device
+ * computes its row block from its resident shard. */
+ngemm_status ngemm_cuda_gemm_packed_multi(const ngemm_packed_handle* shards, int ndev, const int8_t* b,
+                                          int32_t* c, int64_t n, int sat_mode);
 
 /* ---- GPU autotuner (replaces the CPU tile search of tuner.hpp:132-245) -------------------- */
 typedef struct {

@@ -23,7 +23,7 @@ EXPORTS = [
     "ngemm_cuda_gemm_packed_resident_host", "ngemm_cuda_device", "ngemm_cuda_tune", "ngemm_cuda_tune_store_save",
     "ngemm_cuda_tune_store_load", "ngemm_cuda_tune_clear", "ngemm_cuda_gemm_u8i8_strided_batched",
     "ngemm_cuda_gemm_u8i8_requant", "ngemm_cuda_set_option", "ngemm_cuda_get_option", "ngemm_cuda_reset_options",
-    "ngemm_cuda_trim",
+    "ngemm_cuda_trim", "ngemm_cuda_packed_upload_sharded", "ngemm_cuda_gemm_packed_multi",
 ]
 
 OK, ERR_SHAPE, ERR_UNSUPPORTED, ERR_CONFIG, ERR_RANGE, ERR_CORRUPTION, ERR_INDEX, ERR_CUDA, ERR_TUNE = range(9)
@@ -93,6 +93,9 @@ def load():
         L.ngemm_cuda_get_option.argtypes = [C.c_char_p]
         L.ngemm_cuda_reset_options.argtypes = []
         L.ngemm_cuda_trim.argtypes = []
+        L.ngemm_cuda_packed_upload_sharded.argtypes = [C.POINTER(PackedMeta), vp, C.c_size_t, C.POINTER(i32), i32,
+                                                       C.POINTER(vp)]
+        L.ngemm_cuda_gemm_packed_multi.argtypes = [C.POINTER(vp), i32, vp, vp, i64, i32]
         for f in EXPORTS:
             fn = getattr(L, f)
             if f not in ("ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error",

@@ -408,6 +408,44 @@ def gemm_multi(devices, a: np.ndarray, b: np.ndarray, mode: SatMode, gather_devi
     return (c, g.value) if gather_device >= 0 else c
 
 
+class ShardedPackedWeight:
+    """A packed weight split by rows over several GPUs and kept resident there (whole tm-strips
+    per device; ngemm_cuda_packed_upload_sharded)."""
+
+    def __init__(self, p: PackedWeight, devices):
+        self.devices = list(devices)
+        self.m, self.k = p.m_orig, p.k_orig
+        data = np.ascontiguousarray(p.data)
+        meta = p.meta()
+        devs = (C.c_int * len(self.devices))(*self.devices)
+        self.h = (C.c_void_p * len(self.devices))()
+        check(_lib.load().ngemm_cuda_packed_upload_sharded(C.byref(meta), data.ctypes.data, data.nbytes, devs,
+                                                             len(self.devices), self.h))
+
+    def gemm(self, b: np.ndarray, mode: SatMode) -> np.ndarray:
+        """gemm_ngemm on the sharded weight: host B in, host C out (B replicated over NVLink)."""
+        b = np.ascontiguousarray(b)
+        if b.dtype != np.int8 or b.ndim != 2 or b.shape[1] != self.k:
+            raise ShapeError(f"sharded gemm: B must be int8 [N, {self.k}]")
+        c = np.empty((self.m, b.shape[0]), np.int32)
+        check(_lib.load().ngemm_cuda_gemm_packed_multi(self.h, len(self.devices), b.ctypes.data, c.ctypes.data,
+                                                         b.shape[0], int(mode)))
+        return c
+
+    def free(self):
+        L = _lib.load()
+        for i in range(len(self.devices)):
+            if self.h[i]:
+                L.ngemm_cuda_packed_free(self.h[i])
+                self.h[i] = None
+
+    def __del__(self):
+        try:
+            self.free()
+        except Exception:
+            pass
+
+
 def tune(m: int, n: int, k: int, mode: SatMode, repeats: int = 5, warmup: int = 2) -> dict:
     """GPU autotuner (the reference's tune(), tuner.hpp:132-175, re-targeted): every applicable
     kernel configuration is verified bit-for-bit against the CUDA-core reference kernel, then

@@ -192,13 +192,31 @@ void give_slots(std::vector<Slot>& s) {
     s.clear();
 }
 
+// rows x cols int32 block (row pitch n on both sides) from this device to `dst` on device dst_dev:
+// one peer copy when the block is whole rows, else a 2-D copy (UVA: peer access makes the pointer
+// addressable, cudaMemcpy2DAsync with cudaMemcpyDefault moves it over NVLink).
+cudaError_t cudaMemcpy2DPeerAsync_compat(int32_t* dst, int dst_dev, const int32_t* src, int64_t n, int64_t cols,
+                                         int64_t rows, cudaStream_t st) {
+    int src_dev = 0;
+    cudaGetDevice(&src_dev);
+    if (cols == n)
+        return cudaMemcpyPeerAsync(dst, dst_dev, src, src_dev, static_cast<size_t>(rows * n) * 4, st);
+    return cudaMemcpy2DAsync(dst, static_cast<size_t>(n) * 4, src, static_cast<size_t>(n) * 4, static_cast<size_t>(cols) * 4,
+                             static_cast<size_t>(rows), cudaMemcpyDefault, st);
+}
+
 // ---------------------------------------------------------------- the pipeline
 struct HostGemm {
     const uint8_t* a_host = nullptr;  // A rows on the host (k bytes each), or
     const uint8_t* a_dev = nullptr;   // device-resident A (lda_dev pitch)
     int64_t lda_dev = 0;
-    const int8_t* b_host = nullptr;
-    int32_t* c_host = nullptr;
+    const int8_t* b_host = nullptr;   // B rows on the host, or
+    const int8_t* b_dev = nullptr;    // device-resident B (ldb_dev pitch; the multi-GPU replica)
+    int64_t ldb_dev = 0;
+    cudaEvent_t b_ready = nullptr;    // recorded once b_dev holds B (may be null)
+    int32_t* c_host = nullptr;        // host C (may be null when only gathering), and/or
+    int32_t* c_gather = nullptr;      // a device buffer (row pitch n) on device gather_dev: C rows
+    int gather_dev = -1;              // are peer-copied there tile by tile (NVLink)
     bool a_pinned = false, b_pinned = false, c_pinned = false;
     int64_t m = 0, n = 0, k = 0;
     int mode = 0, kernel = 0;
@@ -219,12 +237,14 @@ std::vector<std::pair<int64_t, int64_t>> blocks_growing(int64_t total, int64_t f
 ngemm_status host_pipeline(const HostGemm& g) {
     const int64_t m = g.m, n = g.n, k = g.k;
     const int64_t kp = round_up(k, 16);
-    const bool a_res = g.a_dev != nullptr;
+    const bool a_res = g.a_dev != nullptr, b_res = g.b_dev != nullptr;
     // tile grid: column blocks (B rows) x row blocks (A rows)
     const int64_t rfull = round_up((m + 7) / 8, 256), cfull = round_up((n + 3) / 4, 256);
     const auto rows = a_res ? blocks_growing(m, rfull, rfull, 256) : blocks_growing(m, 256, rfull, 256);
     std::vector<std::pair<int64_t, int64_t>> cols;
-    {
+    if (b_res) {
+        cols.push_back({0, n});  // B resident: full-width row tiles, contiguous C copies
+    } else {
         // streamed A: pass 0 must out-produce A's arrival by enough C backlog to cover B_1's load
         // (w0 >= 5K/16: 1.25 bytes of C per byte of A)
         const int64_t w0 = a_res ? std::min<int64_t>(1024, cfull) : std::max<int64_t>(cfull, round_up(5 * k / 16, 256));
@@ -236,11 +256,11 @@ ngemm_status host_pipeline(const HostGemm& g) {
         }
     }
     const int ti = static_cast<int>(rows.size()), tj = static_cast<int>(cols.size());
-    const bool stage_in = (!a_res && !g.a_pinned) || !g.b_pinned;
-    const bool stage_out = !g.c_pinned;
+    const bool stage_in = (!a_res && !g.a_pinned) || (!b_res && !g.b_pinned);
+    const bool stage_out = g.c_host != nullptr && !g.c_pinned;
     if ((stage_in || stage_out) && kp > static_cast<int64_t>(kSlotBytes)) return NGEMM_ERR_UNSUPPORTED;  // caller falls back
 
-    const size_t a_bytes = a_res ? 0 : static_cast<size_t>(m * kp), b_bytes = static_cast<size_t>(n * kp);
+    const size_t a_bytes = a_res ? 0 : static_cast<size_t>(m * kp), b_bytes = b_res ? 0 : static_cast<size_t>(n * kp);
     const size_t c_bytes = static_cast<size_t>(m * n) * 4;
     const size_t b_off = round_up(static_cast<int64_t>(a_bytes), 256), c_off = b_off + round_up(b_bytes, 256);
     cudaStream_t sin = nullptr, scomp = nullptr, sout = nullptr;
@@ -341,23 +361,26 @@ ngemm_status host_pipeline(const HostGemm& g) {
             const int64_t c0 = cols[j].first, ncols = cols[j].second;
             for (int i = 0; i < ti; ++i, ++t) {
                 const int64_t r0 = rows[i].first, nrows = rows[i].second;
-                if (s == NGEMM_OK && i == 0) {
+                if (s == NGEMM_OK && i == 0 && !b_res) {
                     h2d_rows(buf + b_off + c0 * kp, g.b_host + c0 * k, ncols, g.b_pinned);
                     ck(cudaEventRecord(ev[ti + j], sin), "record");
                 }
+                if (s == NGEMM_OK && t == 0 && b_res && g.b_ready) ck(cudaStreamWaitEvent(scomp, g.b_ready, 0), "wait");
                 if (s == NGEMM_OK && j == 0 && !a_res) {
                     h2d_rows(buf + r0 * kp, g.a_host + r0 * k, nrows, g.a_pinned);
                     ck(cudaEventRecord(ev[i], sin), "record");
                 }
                 if (s == NGEMM_OK) {
                     if (!a_res) ck(cudaStreamWaitEvent(scomp, ev[i], 0), "wait");
-                    ck(cudaStreamWaitEvent(scomp, ev[ti + j], 0), "wait");
+                    if (!b_res) ck(cudaStreamWaitEvent(scomp, ev[ti + j], 0), "wait");
                 }
                 if (s == NGEMM_OK) {
                     const uint8_t* ablk = a_res ? g.a_dev + r0 * g.lda_dev : buf + r0 * kp;
                     const int64_t lda = a_res ? g.lda_dev : kp;
-                    ngemm_status gs = run_gemm(ablk, lda, reinterpret_cast<const int8_t*>(buf + b_off + c0 * kp), kp,
-                                               dc + r0 * n + c0, n, nrows, ncols, k, g.mode, g.kernel, scomp);
+                    const int8_t* bblk = b_res ? g.b_dev + c0 * g.ldb_dev : reinterpret_cast<const int8_t*>(buf + b_off + c0 * kp);
+                    const int64_t ldb = b_res ? g.ldb_dev : kp;
+                    ngemm_status gs = run_gemm(ablk, lda, bblk, ldb, dc + r0 * n + c0, n, nrows, ncols, k, g.mode, g.kernel,
+                                               scomp);
                     if (gs != NGEMM_OK) {
                         std::lock_guard<std::mutex> lk(err_mu);
                         if (s == NGEMM_OK) s = gs;
@@ -365,7 +388,12 @@ ngemm_status host_pipeline(const HostGemm& g) {
                 }
                 cudaEvent_t ev_c = ev[ti + tj + t];
                 if (s == NGEMM_OK) ck(cudaEventRecord(ev_c, scomp), "record");
-                if (s == NGEMM_OK && !stage_out) {
+                if (s == NGEMM_OK && g.c_gather) {  // C rows assembled on the gather device (NVLink peer copy)
+                    ck(cudaStreamWaitEvent(sout, ev_c, 0), "wait");
+                    ck(cudaMemcpy2DPeerAsync_compat(g.c_gather + r0 * n + c0, g.gather_dev, dc + r0 * n + c0, n, ncols,
+                                                    nrows, sout), "peer gather");
+                }
+                if (s == NGEMM_OK && g.c_host && !stage_out) {
                     ck(cudaStreamWaitEvent(sout, ev_c, 0), "wait");
                     if (tj == 1)
                         ck(cudaMemcpyAsync(g.c_host + r0 * n, dc + r0 * n, static_cast<size_t>(nrows * n) * 4,

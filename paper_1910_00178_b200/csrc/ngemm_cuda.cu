@@ -1624,6 +1624,174 @@ ngemm_status ngemm_cuda_shard_rows(int64_t m, int ndev, int64_t align, int64_t* 
     return NGEMM_OK;
 }
 
+}  // extern "C"
+
+namespace {
+
+// Peer access between every pair of distinct devices in the list (NVLink / NVSwitch), once per
+// process and pair; a pair without P2P keeps working (copies are then staged by the driver).
+void enable_peers(const int* devices, int ndev) {
+    static std::mutex mu;
+    static std::vector<std::pair<int, int>> done;
+    std::lock_guard<std::mutex> lk(mu);
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (int i = 0; i < ndev; ++i)
+        for (int j = 0; j < ndev; ++j) {
+            const int a = devices[i], b = devices[j];
+            if (a == b || std::find(done.begin(), done.end(), std::make_pair(a, b)) != done.end()) continue;
+            done.push_back({a, b});
+            int can = 0;
+            if (cudaDeviceCanAccessPeer(&can, a, b) != cudaSuccess || !can) {
+                cudaGetLastError();
+                continue;
+            }
+            cudaSetDevice(a);
+            if (cudaDeviceEnablePeerAccess(b, 0) != cudaSuccess) cudaGetLastError();  // already enabled is fine
+        }
+    cudaSetDevice(prev);
+}
+
+// Replicas of one host buffer (rows x k bytes, row pitch kp on the devices) on every device: ONE
+// host-to-device copy into devices[0], then a chunked relay devices[0] -> [1] -> ... over NVLink
+// (each chunk is forwarded as soon as it lands), so PCIe carries B once and the replication costs
+// about one chunk per extra device.  ready[d] is recorded on device d once its replica is whole.
+struct Replicas {
+    std::vector<uint8_t*> ptr;
+    std::vector<cudaStream_t> st;
+    std::vector<cudaEvent_t> ready;
+};
+ngemm_status replicate_rows(const int* devices, int ndev, const void* host, int64_t rows, int64_t k, int64_t kp,
+                            Replicas* r) {
+    r->ptr.assign(ndev, nullptr);
+    r->st.assign(ndev, nullptr);
+    r->ready.assign(ndev, nullptr);
+    const int64_t chunk = std::max<int64_t>(1, (16 << 20) / kp);
+    const int64_t nchunks = (rows + chunk - 1) / chunk;
+    std::vector<std::vector<cudaEvent_t>> landed(ndev, std::vector<cudaEvent_t>(static_cast<size_t>(nchunks), nullptr));
+    ngemm_status s = NGEMM_OK;
+    for (int d = 0; d < ndev && s == NGEMM_OK; ++d) {
+        if (cudaSetDevice(devices[d]) != cudaSuccess ||
+            cudaStreamCreateWithFlags(&r->st[d], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaEventCreateWithFlags(&r->ready[d], cudaEventDisableTiming) != cudaSuccess ||
+            dev_alloc(&r->ptr[d], static_cast<size_t>(rows * kp), r->st[d]) != cudaSuccess) {
+            s = fail(NGEMM_ERR_CUDA, "replicate: device setup failed on device " + std::to_string(devices[d]));
+            break;
+        }
+        for (auto& e : landed[d])
+            if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) s = fail(NGEMM_ERR_CUDA, "event");
+    }
+    for (int64_t c = 0; c < nchunks && s == NGEMM_OK; ++c) {
+        const int64_t r0 = c * chunk, nr = std::min(chunk, rows - r0);
+        for (int d = 0; d < ndev && s == NGEMM_OK; ++d) {
+            cudaSetDevice(devices[d]);
+            cudaError_t e;
+            if (d == 0) {
+                e = copy_rows_h2d(r->ptr[0] + r0 * kp, kp, static_cast<const uint8_t*>(host) + r0 * k, k, nr, r->st[0]);
+            } else {
+                cudaStreamWaitEvent(r->st[d], landed[d - 1][c], 0);
+                e = cudaMemcpyPeerAsync(r->ptr[d] + r0 * kp, devices[d], r->ptr[d - 1] + r0 * kp, devices[d - 1],
+                                        static_cast<size_t>(nr * kp), r->st[d]);
+            }
+            if (e != cudaSuccess) s = fail(NGEMM_ERR_CUDA, std::string("replicate: ") + cudaGetErrorString(e));
+            else cudaEventRecord(landed[d][c], r->st[d]);
+        }
+    }
+    for (int d = 0; d < ndev && s == NGEMM_OK; ++d) {
+        cudaSetDevice(devices[d]);
+        cudaEventRecord(r->ready[d], r->st[d]);
+    }
+    // chunk events may be destroyed right after their records are enqueued (the driver releases
+    // them once they complete); on failure drain the relay before the caller frees the replicas
+    for (int d = 0; d < ndev; ++d) {
+        if (!r->st[d]) continue;
+        cudaSetDevice(devices[d]);
+        if (s != NGEMM_OK) cudaStreamSynchronize(r->st[d]);
+        for (auto& e : landed[d])
+            if (e) cudaEventDestroy(e);
+    }
+    return s;
+}
+
+void free_replicas(const int* devices, int ndev, Replicas* r) {
+    for (int d = 0; d < ndev && d < static_cast<int>(r->ptr.size()); ++d) {
+        cudaSetDevice(devices[d]);
+        if (r->ptr[d]) cudaFreeAsync(r->ptr[d], r->st[d]);
+        if (r->st[d]) {
+            cudaStreamSynchronize(r->st[d]);
+            cudaStreamDestroy(r->st[d]);
+        }
+        if (r->ready[d]) cudaEventDestroy(r->ready[d]);
+    }
+}
+
+// One host thread per device running the host pipeline on its row shard (A rows streamed in,
+// the replicated B resident, C rows streamed out to the host and/or peer-copied to the gather
+// buffer).  `a_dev` (per device) replaces the host A for resident sharded weights.
+ngemm_status run_multi(const int* devices, int ndev, const std::vector<int64_t>& rs, const uint8_t* a_host,
+                       const std::vector<const uint8_t*>& a_dev, const std::vector<int64_t>& lda_dev, const int8_t* b,
+                       int32_t* c, int64_t n, int64_t k, int sat_mode, int gather_device, int32_t* full) {
+    enable_peers(devices, ndev);
+    if (gather_device >= 0) {
+        std::vector<int> all(devices, devices + ndev);
+        all.push_back(gather_device);
+        enable_peers(all.data(), ndev + 1);
+    }
+    const int64_t kp = round_up(k, 16);
+    Replicas rep;
+    ngemm_status s = replicate_rows(devices, ndev, b, n, k, kp, &rep);
+    std::vector<ngemm_status> st(static_cast<size_t>(ndev), NGEMM_OK);
+    std::vector<std::string> msg(static_cast<size_t>(ndev));
+    if (s == NGEMM_OK) {
+        const bool a_pinned = a_host && is_pinned(a_host), b_pinned = is_pinned(b), c_pinned = c && is_pinned(c);
+        std::vector<std::thread> workers;
+        for (int d = 0; d < ndev; ++d) {
+            workers.emplace_back([&, d] {
+                const int64_t r0 = rs[d], rows = rs[d + 1] - rs[d];
+                if (rows <= 0) return;
+                if (cudaSetDevice(devices[d]) != cudaSuccess) {
+                    st[d] = fail(NGEMM_ERR_CUDA, "cudaSetDevice failed");
+                    msg[d] = ngemm_cuda_last_error();
+                    return;
+                }
+                HostGemm g;
+                if (!a_dev.empty()) {
+                    g.a_dev = a_dev[d];
+                    g.lda_dev = lda_dev[d];
+                } else {
+                    g.a_host = a_host + r0 * k;
+                    g.a_pinned = a_pinned;
+                }
+                g.b_dev = reinterpret_cast<const int8_t*>(rep.ptr[d]);
+                g.ldb_dev = kp;
+                g.b_ready = rep.ready[d];
+                g.b_pinned = b_pinned;
+                g.c_host = c ? c + r0 * n : nullptr;
+                g.c_pinned = c_pinned;
+                g.c_gather = full ? full + r0 * n : nullptr;
+                g.gather_dev = gather_device;
+                g.m = rows;
+                g.n = n;
+                g.k = k;
+                g.mode = sat_mode;
+                g.kernel = NGEMM_KERNEL_AUTO;
+                st[d] = host_pipeline(g);
+                if (st[d] != NGEMM_OK) msg[d] = st[d] == NGEMM_ERR_UNSUPPORTED ? "row too long for staging" : ngemm_cuda_last_error();
+            });
+        }
+        for (auto& w : workers) w.join();
+    }
+    free_replicas(devices, ndev, &rep);
+    if (s != NGEMM_OK) return s;
+    for (int d = 0; d < ndev; ++d)
+        if (st[d] != NGEMM_OK) return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
+    return NGEMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
 ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint8_t* a, const int8_t* b, int32_t* c,
                                         int64_t m, int64_t n, int64_t k, int sat_mode, int gather_device,
                                         int32_t** gathered) {
@@ -1633,6 +1801,7 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
     ngemm_status s = validate(a, k, b, k, c ? static_cast<const void*>(c) : static_cast<const void*>(a), n, m, n, k,
                               sat_mode);
     if (s != NGEMM_OK) return s;
+    if (round_up(k, 16) > static_cast<int64_t>(kSlotBytes)) return fail(NGEMM_ERR_SHAPE, "multi: K too large");
     std::vector<int64_t> rs(static_cast<size_t>(ndev) + 1);
     ngemm_cuda_shard_rows(m, ndev, tc::BM, rs.data());
     int prev = 0;
@@ -1642,76 +1811,101 @@ ngemm_status ngemm_cuda_gemm_u8i8_multi(const int* devices, int ndev, const uint
         NG_CUDA(cudaSetDevice(gather_device));
         NG_CUDA(cudaMalloc(&full, static_cast<size_t>(m * n) * 4));
     }
-    // One host thread per device: H2D of the row shard of A and a replica of B, the GEMM on the
-    // device's own stream, then C rows to the host and/or peer-copied (NVLink) into the gather
-    // buffer — shards of row-major C are contiguous, so the gather is a pure concatenation.
-    std::vector<ngemm_status> st(static_cast<size_t>(ndev), NGEMM_OK);
-    std::vector<std::string> msg(static_cast<size_t>(ndev));
-    std::vector<std::thread> workers;
-    for (int d = 0; d < ndev; ++d) {
-        workers.emplace_back([&, d] {
-            const int64_t r0 = rs[d], r1 = rs[d + 1], rows = r1 - r0;
-            if (rows <= 0) return;
-            auto bad = [&](ngemm_status code, const std::string& what) {
-                st[d] = code;
-                msg[d] = what;
-            };
-            if (cudaSetDevice(devices[d]) != cudaSuccess) return bad(NGEMM_ERR_CUDA, "cudaSetDevice failed");
-            int dev;
-            DevInfo di;
-            if (current_device(&dev, &di) != NGEMM_OK) return bad(NGEMM_ERR_CUDA, ngemm_cuda_last_error());
-            const int64_t kp = round_up(k, 16);
-            const size_t a_b = static_cast<size_t>(rows * kp), b_b = static_cast<size_t>(n * kp);
-            const size_t c_b = static_cast<size_t>(rows * n) * 4;
-            const size_t b_off = round_up(static_cast<int64_t>(a_b), 256), c_off = b_off + round_up(static_cast<int64_t>(b_b), 256);
-            cudaStream_t stream = nullptr;
-            if (cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking) != cudaSuccess)
-                return bad(NGEMM_ERR_CUDA, "stream create failed");
-            uint8_t* buf = nullptr;
-            ngemm_status ls = NGEMM_OK;
-            if (dev_alloc(&buf, c_off + c_b, stream) != cudaSuccess) {
-                ls = NGEMM_ERR_CUDA;
-                msg[d] = "device allocation failed";
-            }
-            int32_t* dc = buf ? reinterpret_cast<int32_t*>(buf + c_off) : nullptr;
-            if (ls == NGEMM_OK && (copy_rows_h2d(buf, kp, a + r0 * k, k, rows, stream) != cudaSuccess ||
-                                   copy_rows_h2d(buf + b_off, kp, b, k, n, stream) != cudaSuccess)) {
-                ls = NGEMM_ERR_CUDA;
-                msg[d] = "H2D copy failed";
-            }
-            if (ls == NGEMM_OK) {
-                ls = run_gemm(buf, kp, reinterpret_cast<const int8_t*>(buf + b_off), kp, dc, n, rows, n, k, sat_mode,
-                              NGEMM_KERNEL_AUTO, stream);
-                if (ls != NGEMM_OK) msg[d] = ngemm_cuda_last_error();
-            }
-            if (ls == NGEMM_OK && c &&
-                cudaMemcpyAsync(c + r0 * n, dc, c_b, cudaMemcpyDeviceToHost, stream) != cudaSuccess) {
-                ls = NGEMM_ERR_CUDA;
-                msg[d] = "D2H copy failed";
-            }
-            if (ls == NGEMM_OK && full &&
-                cudaMemcpyPeerAsync(full + r0 * n, gather_device, dc, devices[d], c_b, stream) != cudaSuccess) {
-                ls = NGEMM_ERR_CUDA;
-                msg[d] = "peer gather copy failed";
-            }
-            if (buf) cudaFreeAsync(buf, stream);
-            if (cudaStreamSynchronize(stream) != cudaSuccess && ls == NGEMM_OK) {
-                ls = NGEMM_ERR_CUDA;
-                msg[d] = cudaGetErrorString(cudaGetLastError());
-            }
-            cudaStreamDestroy(stream);
-            st[d] = ls;
-        });
-    }
-    for (auto& w : workers) w.join();
-    cudaSetDevice(prev);
-    for (int d = 0; d < ndev; ++d)
-        if (st[d] != NGEMM_OK) {
-            if (full) cudaFree(full);
-            return fail(st[d], "device " + std::to_string(devices[d]) + ": " + msg[d]);
+    s = run_multi(devices, ndev, rs, a, {}, {}, b, c, n, k, sat_mode, want_gather ? gather_device : -1, full);
+    if (full) {  // gather copies ran on the workers' streams, which host_pipeline synchronised
+        cudaSetDevice(gather_device);
+        if (s != NGEMM_OK) {
+            cudaFree(full);
+            full = nullptr;
         }
+    }
+    cudaSetDevice(prev);
+    if (s != NGEMM_OK) return s;
     if (want_gather) *gathered = full;
     return NGEMM_OK;
+}
+
+// Sharded resident weight: the packed weight's rows split over `devices` in tile-aligned blocks
+// of whole tm-strips (ngemm_cuda_shard_rows with align = lcm(tm, 128)).  With an M-before-K
+// permutation each strip is one contiguous byte range (layout.hpp:159-161), so a shard is a plain
+// copy of the packed bytes; with K-before-M each K tile row contributes one contiguous run of the
+// shard's strips, gathered on the host.  Each shard is then repacked on its device.
+ngemm_status ngemm_cuda_packed_upload_sharded(const ngemm_packed_meta* meta, const uint8_t* host_packed, size_t nbytes,
+                                              const int* devices, int ndev, ngemm_packed_handle* out) {
+    ngemm_status s = validate_meta(meta);
+    if (s != NGEMM_OK) return s;
+    if (!devices || ndev < 1 || !out || !host_packed) return fail(NGEMM_ERR_CONFIG, "upload_sharded: bad arguments");
+    if (meta->h != 4) return fail(NGEMM_ERR_UNSUPPORTED, "upload_sharded: u8 weights only");
+    if (nbytes != static_cast<size_t>(meta->m_pad * meta->k_pad))
+        return fail(NGEMM_ERR_SHAPE, "upload_sharded: byte size disagrees with m_pad*k_pad");
+    const int64_t tm = meta->tm, tk = meta->tk;
+    int64_t align = 128;
+    while (align % tm) align += 128;  // lcm(tm, 128)
+    std::vector<int64_t> rs(static_cast<size_t>(ndev) + 1);
+    ngemm_cuda_shard_rows(meta->m_orig, ndev, align, rs.data());
+    const bool m_first = meta->perm == 0 || meta->perm == 1 || meta->perm == 2;
+    const int64_t n_tm = meta->m_pad / tm, n_tk = meta->k_pad / tk, tile_bytes = tm * tk;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    for (int d = 0; d < ndev; ++d) out[d] = nullptr;
+    std::vector<uint8_t> gathered;
+    for (int d = 0; d < ndev && s == NGEMM_OK; ++d) {
+        const int64_t rows = rs[d + 1] - rs[d];
+        if (rows <= 0) continue;
+        const int64_t s0 = rs[d] / tm, s1 = (rs[d] + round_up(rows, tm)) / tm;  // strips [s0, s1)
+        ngemm_packed_meta sm = *meta;
+        sm.m_orig = rows;
+        sm.m_pad = (s1 - s0) * tm;
+        const uint8_t* src;
+        if (m_first) {
+            src = host_packed + s0 * n_tk * tile_bytes;
+        } else {
+            gathered.resize(static_cast<size_t>(sm.m_pad * meta->k_pad));
+            for (int64_t t = 0; t < n_tk; ++t)
+                std::memcpy(gathered.data() + t * (s1 - s0) * tile_bytes, host_packed + (t * n_tm + s0) * tile_bytes,
+                            static_cast<size_t>((s1 - s0) * tile_bytes));
+            src = gathered.data();
+        }
+        if (cudaSetDevice(devices[d]) != cudaSuccess) s = fail(NGEMM_ERR_CUDA, "cudaSetDevice failed");
+        if (s == NGEMM_OK) s = ngemm_cuda_packed_upload(&sm, src, static_cast<size_t>(sm.m_pad * sm.k_pad), &out[d]);
+    }
+    cudaSetDevice(prev);
+    if (s != NGEMM_OK)
+        for (int d = 0; d < ndev; ++d) {
+            ngemm_cuda_packed_free(out[d]);
+            out[d] = nullptr;
+        }
+    return s;
+}
+
+// gemm_ngemm over a sharded resident weight: B replicated by one H2D + NVLink relay, every
+// device computes its rows of C from its resident shard, C rows stream back to the host.
+ngemm_status ngemm_cuda_gemm_packed_multi(const ngemm_packed_handle* shards, int ndev, const int8_t* b, int32_t* c,
+                                          int64_t n, int sat_mode) {
+    if (!shards || ndev < 1 || !b || !c) return fail(NGEMM_ERR_SHAPE, "packed_multi: bad arguments");
+    std::vector<int> devices;
+    std::vector<const uint8_t*> a_dev;
+    std::vector<int64_t> lda, rs{0};
+    int64_t k = -1;
+    for (int d = 0; d < ndev; ++d) {
+        if (!shards[d]) continue;  // an empty shard (more devices than row blocks)
+        if (shards[d]->esize != 1) return fail(NGEMM_ERR_UNSUPPORTED, "packed_multi: u8 weights only");
+        if (k >= 0 && shards[d]->k != k) return fail(NGEMM_ERR_SHAPE, "packed_multi: shards disagree on K");
+        k = shards[d]->k;
+        devices.push_back(shards[d]->device);
+        a_dev.push_back(shards[d]->d_a);
+        lda.push_back(shards[d]->lda);
+        rs.push_back(rs.back() + shards[d]->m);
+    }
+    if (devices.empty()) return fail(NGEMM_ERR_SHAPE, "packed_multi: no shards");
+    ngemm_status s = validate(a_dev[0], lda[0], b, k, c, n, rs.back(), n, k, sat_mode);
+    if (s != NGEMM_OK) return s;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    s = run_multi(devices.data(), static_cast<int>(devices.size()), rs, nullptr, a_dev, lda, b, c, n, k, sat_mode, -1,
+                  nullptr);
+    cudaSetDevice(prev);
+    return s;
 }
 
 // ---------------------------------------------------------------- GPU autotuner (tuner.hpp:132-245)

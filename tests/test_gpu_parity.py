@@ -3,6 +3,7 @@ against the CPU oracle (pinned to the reference) and the reference-generated fix
 
 Modes: SAT = HardwareSaturating (gemm_sat_oracle, gemm.hpp:83-104), EXACT = WideningExact
 (gemm_ref, gemm.hpp:36-52).  Integer work: the bar is bit-exact, no tolerance."""
+import ctypes
 import os
 
 import numpy as np
@@ -281,6 +282,38 @@ def _c5_row_blocks(m, block=64, count=8, seed=5):
     while len(starts) < count:
         starts.add(int(rng.integers(1, (m - block) // block)) * block)
     return sorted(starts)
+
+
+def test_multi_device_driver_pipeline_and_sharded_weight(cuda, oracle):
+    """The multi-GPU entries on one GPU listed several times (each listing = one row shard; the
+    NVLink relay of B becomes device-local copies): B copied once and relayed, A rows streamed in
+    and C rows out through the host pipeline (pageable and pinned), the peer-copy gather, and
+    the sharded resident weight for every permutation (M-before-K shards are plain byte ranges,
+    K-before-M shards are gathered per K tile row)."""
+    import torch
+    for (m, n, k) in [(1000, 900, 333), (3000, 4100, 1024)]:
+        a = oracle.mat_random_u8(m, k, 41)
+        b = oracle.mat_random_i8(n, k, 42)
+        for mode in (EXACT, SAT):
+            ref = oracle.gemm(a, b, mode)
+            assert (api.gemm_multi([0, 0, 0], a, b, mode) == ref).all(), (m, n, k, mode)
+            ta, tb = torch.from_numpy(a).pin_memory(), torch.from_numpy(b).pin_memory()
+            tc = torch.full((m, n), -1, dtype=torch.int32).pin_memory()
+            devs = (ctypes.c_int * 4)(0, 0, 0, 0)
+            _lib.check(_lib.load().ngemm_cuda_gemm_u8i8_multi(devs, 4, ta.data_ptr(), tb.data_ptr(), tc.data_ptr(),
+                                                              m, n, k, mode, -1, None))
+            assert (tc.numpy() == ref).all(), ("pinned", m, n, k, mode)
+    a = oracle.mat_random_u8(1500, 640, 43)
+    b = oracle.mat_random_i8(700, 640, 44)
+    for perm in range(6):
+        p = api.pack_weights(a, api.KernelShape(64, 4, 16), api.TileConfig(32, 64, 64, api.Perm(perm)))
+        for devs in ([0], [0, 0], [0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0]):  # the last: more devices than blocks
+            w = api.ShardedPackedWeight(p, devs)
+            try:
+                for mode in (EXACT, SAT):
+                    assert (w.gemm(b, mode) == oracle.gemm(a, b, mode)).all(), (perm, len(devs), mode)
+            finally:
+                w.free()
 
 
 @pytest.mark.slow

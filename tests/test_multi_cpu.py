@@ -1,4 +1,4 @@
-"""Multi-process (world size 2, gloo, CPU) coverage of the M-shard path's host logic: row
+"""Multi-process (world sizes 2 and 4, gloo, CPU) coverage of the M-shard path's host logic: row
 blocks, per-rank work on the local block (computed here by the CPU oracle, standing in for the
 GPU kernel), max-over-ranks timing and the gather of C — compared with the unsharded oracle."""
 import os
@@ -46,9 +46,11 @@ def _worker(rank, world, port, m, n, k, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("m", [300, 1000, 100])
-def test_m_shard_world2_gloo(m):
-    world, n, k = 2, 70, 96
+@pytest.mark.parametrize("world,m", [(2, 300), (2, 1000), (2, 100), (4, 1000), (4, 300), (4, 100)])
+def test_m_shard_gloo(world, m):
+    """World sizes 2 and 4 with ragged row blocks (1000 rows over 4 ranks: 256/256/256/232) and
+    ranks that own no rows at all (100 rows over 4 ranks)."""
+    n, k = 70, 96
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
