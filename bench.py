@@ -259,9 +259,10 @@ def load_traffic(tag):
 
 
 # bench workload -> the committed ncu --set full summary of its dominant kernel (profiles/)
-NCU_TAGS = {"tcgen05:16384x16384x16384:exact": "c5_tc", "tcgen05:1024x1024x1024:exact": "c1_tc",
-            "tcgen05:2048x4096x1024:exact": "c3_tc", "skinny:16x4096x1024:exact": "c2_mma",
-            "skinny:1x4096x1024:exact": "c2_mma_m1", "skinny:16x4096x1024:sat": "c2_sat"}
+NCU_TAGS = {"tcgen05:16384x16384x16384:exact": "r2/ncu_c5_tc_r2.json", "tcgen05:1024x1024x1024:exact": "r2/ncu_c1_tc_r2.json",
+            "tcgen05:2048x4096x1024:exact": "r2/ncu_c3_tc_r2.json", "tcgen05:2048x2048x2048:exact": "r2/ncu_c4_tc_r2.json",
+            "skinny:16x4096x1024:exact": "r2/ncu_c2_mma_r2.json", "skinny:1x4096x1024:exact": "ncu_c2_mma_m1.json",
+            "skinny:16x4096x1024:sat": "r2/ncu_c2_sat_r2.json"}
 
 
 def load_ncu(tag):
@@ -269,7 +270,7 @@ def load_ncu(tag):
     name = NCU_TAGS.get(tag)
     if not name:
         return None
-    path = os.path.join(ROOT, "profiles", f"ncu_{name}.json")
+    path = os.path.join(ROOT, "profiles", name)
     try:
         with open(path) as f:
             cap = json.load(f)["full_capture"][0]
@@ -280,7 +281,7 @@ def load_ncu(tag):
             "tensor_mem_active_pct": "sm__mem_tensor_cycles_active.avg.pct_of_peak_sustained_active",
             "dram_read": "dram__bytes_read.sum", "dram_write": "dram__bytes_write.sum"}
     out = {k: cap[v] for k, v in pick.items() if v in cap}
-    out["file"] = f"profiles/ncu_{name}.json"
+    out["file"] = f"profiles/{name}"
     return out
 
 

@@ -63,7 +63,7 @@ struct TileMap {
     int tiles_m, tiles_n, splits;  // tiles_m counts 128*CG-row tiles
     int group_m;                   // rasterisation: group_m M-tiles walked down before moving along N
     int preissue;                  // 1-CTA tiles: issue the first STAGES loads before the block sync
-    int l2hint;                    // L2 eviction hints: bit 0 A evict_last, bit 1 B evict_first
+    int l2hint;                    // L2 eviction hints: bit 0 A evict_last, bit 1 B evict_first, bit 2 C evict_first
     int prefetch;                  // warm L2 with the first operand slabs before the PDL wait
     int dbg;                       // probes only (NGEMM_TC_DBG): bit 0 skip C stores, bit 1 skip MMAs,
                                    // bit 2 skip operand loads (1-CTA configs)
@@ -281,6 +281,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     } else if (warp >= 4) {
         // ---------------- epilogue (both CTAs): TMEM -> registers -> swizzled smem -> TMA store
         const int ew = warp & 3;  // TMEM lane quadrant this warp may access
+        // C is written once and never re-read by this kernel: map.l2hint bit 2 streams it through
+        // L2 with evict_first so it does not push out the operand slabs the next waves re-read
+        const uint64_t pol_c = policy_evict_first();
         uint8_t* stage_c = smem + S::C_OFFSET + ew * 2 * S::STAGE_C_BYTES;
         int acc = 0, cbuf = 0;
         uint32_t acc_ph = 0;
@@ -349,7 +352,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     fence_proxy_async_smem();
                     __syncwarp();
                     if (lane == 0 && !(map.dbg & 1)) {
-                        if (c_mode == 0) tma_store_2d(&tma_c, buf, col0, row0);
+                        if (c_mode == 0 && (map.l2hint & 4)) tma_store_2d_hint(&tma_c, buf, col0, row0, pol_c);
+                        else if (c_mode == 0) tma_store_2d(&tma_c, buf, col0, row0);
                         else tma_reduce_add_2d(&tma_c, buf, col0, row0);
                         tma_store_commit();
                     }

@@ -126,7 +126,7 @@ struct OptDef {
 constexpr OptDef kOpts[O_N] = {
     {"PDL", 1}, {"L2_PREFETCH", 1}, {"SKINNY_FAST", 1}, {"SKINNY_SPLITS", -1}, {"SKINNY_RG", -1},
     {"SKINNY_WARPS", -1}, {"SKINNY_VARIANT", -1}, {"TC_QUAD", 0}, {"TC_CFG", -1}, {"TC_SPLITS", -1},
-    {"TC_DIRECT", 0}, {"TC_PREISSUE", 0}, {"TC_L2HINT", 3}, {"TC_GROUP_M", -1}, {"TC_DBG", 0},
+    {"TC_DIRECT", 0}, {"TC_PREISSUE", 0}, {"TC_L2HINT", 7}, {"TC_GROUP_M", -1}, {"TC_DBG", 0},
     {"SAT_HYBRID", -1}, {"SATFIX_SKIP", 0}, {"I16_PATH", -1}, {"REQUANT_UNFUSED", 0}, {"TC_SCHED", -1},
 };
 std::atomic<int> g_opt[O_N];
@@ -820,7 +820,7 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.group_m = tc::GROUP_M;
     // pre-issuing the first loads before the block sync measured slower (profiles/ab_preissue_r1.log)
     map.preissue = opt(O_TC_PREISSUE);  // experiments
-    map.l2hint = opt(O_TC_L2HINT);      // experiments (default 3: A evict_last, B evict_first)
+    map.l2hint = opt(O_TC_L2HINT);      // experiments (default 7: A evict_last, B and C evict_first; profiles/r2/l2hint_r2.log)
     map.prefetch = l2_prefetch_enabled() ? 1 : 0;
     map.dbg = 0;
     map.trace_id = -1;
