@@ -10,7 +10,8 @@ import os
 import threading
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libngemm_cuda.so")
+# NGEMM_LIB: an alternative in-tree build of the same library (A/B experiments only)
+LIB_PATH = os.environ.get("NGEMM_LIB") or os.path.join(_HERE, "lib", "libngemm_cuda.so")
 
 # every symbol include/ngemm_cuda.h declares (checked by tests/test_abi.py)
 EXPORTS = [

@@ -470,15 +470,24 @@ namespace ngemm_dev {
 // shuffle levels (transposing, so each lane keeps 1/4 of the values), the CTA's warps meet in
 // shared memory.
 // ---------------------------------------------------------------------------------------------
-template <int MT, int WARPS>
+template <int MT, int WARPS, bool MSPLIT>
 __global__ void __launch_bounds__(WARPS * 32)
     skinny_sat_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                       int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range, int vec_ok,
                       int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc) {
-    constexpr int V = 2 * MT;  // values per thread: rows {g, g+8} x MT
-    __shared__ __align__(16) int32_t red[WARPS * 16 * MT];
+    // MSPLIT: the CTA's warps split A's rows (MS groups of MW <= 4 rows) as well as K (KS warps
+    // per row group), so each warp keeps 2 x MW accumulators and a short unrolled body (its MS - 1
+    // siblings re-read the same B bytes through L1).  It pays when N has few 16-row groups (one
+    // warp per K slice leaves SMs idle and its ~1000-instruction body misses the instruction
+    // cache: 35 % no_instruction stalls, profiles/r2/stalls_c2_sat_r2.txt); with many row groups
+    // the 4x B reads cost more (profiles/r2/skinny_sat_r2.log).
+    constexpr int MW = (MSPLIT && MT > 4) ? 4 : MT, MS = MT / MW, KS = WARPS / MS;
+    static_assert(MT % MW == 0 && WARPS % MS == 0, "warps must split the row groups evenly");
+    constexpr int V = 2 * MW;  // values per thread: rows {g, g+8} x MW
+    __shared__ __align__(16) int32_t red[KS * 16 * MT];
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
+    const int warp_m = warp % MS, warp_k = warp / MS, mb = warp_m * MW;
     pdl_launch_dependents();
     A += blockIdx.z * batch_sa;  // strided batch (blockIdx.z), as in skinny_mma_kernel
     B += blockIdx.z * batch_sb;
@@ -501,17 +510,19 @@ __global__ void __launch_bounds__(WARPS * 32)
     int32_t acc[V];
 #pragma unroll
     for (int i = 0; i < V; ++i) acc[i] = 0;
-    // A row m, half c of the current chunk (aw) against both B rows (bv): 4 K words each
-    auto consume = [&](const uint4 (&bv)[2][2], int m, int c, const uint4& av) {
-        const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
-#pragma unroll
-        for (int r = 0; r < 2; ++r) {
-            const uint32_t bw[4] = {bv[r][c].x, bv[r][c].y, bv[r][c].z, bv[r][c].w};
-            int32_t s = acc[r * MT + m];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) s = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], s);
-            acc[r * MT + m] = s;
-        }
+    // The pair masks go on B (once per chunk, shared by all M rows of A): for a K word with
+    // bytes b0..b3, blo = b & 0xFFFF and bhi = b & 0xFFFF0000, so dp4a(a, blo) = a0 b0 + a1 b1 and
+    // dp4a(a, bhi) = a2 b2 + a3 b3 — the same two pair sums as masking A, one LOP per B word
+    // instead of one per (A word, B row).  Then one I2IP.SAT packs both clamped sums and one
+    // IDP.2A wrap-adds them (sat_word_add's last two steps).
+    auto sat_pairs_add = [](uint32_t a, uint32_t blo, uint32_t bhi, int32_t acc_in) {
+        const int32_t p0 = dp4a_us(a, blo, 0);
+        const int32_t p1 = dp4a_us(a, bhi, 0);
+        uint32_t packed;
+        asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(packed) : "r"(p1), "r"(p0));
+        int32_t r;
+        asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(packed), "r"(0x0101), "r"(acc_in));
+        return r;
     };
 
     const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
@@ -520,39 +531,87 @@ __global__ void __launch_bounds__(WARPS * 32)
     const bool vec = vec_ok != 0, rows_full = n0 + 16 <= N;
     const uint8_t* pb = Bu + (n0 + g) * ldb + t * 16;  // thread t reads bytes [c*64 + t*16, +16) of a chunk
     const uint8_t* pa = A + t * 16;
-#pragma unroll 1
-    for (int64_t ch = warp; ch < chunks; ch += WARPS) {
-        const int64_t k0 = kbeg + ch * 128;  // k_range is a multiple of 128: pairs stay even-aligned
-        uint4 bv[2][2];
-        if ((vec_ok & 4) && rows_full && k0 + 128 <= kend) {
-            // whole chunk in range (warp-uniform): unconditional 16-byte loads
+    // one chunk: B words (2 rows x 2 halves x 4 words) masked once, then every A row against them;
+    // `lb` / `la` load 16 bytes of B / A (unconditional on the fast path, bounded on the ragged one)
+    auto chunk = [&](int64_t k0, auto lb, auto la) {
+        if constexpr (MT == 1 || (MT <= 4 && WARPS >= 32)) {
+            // one A row, or few rows in a 32-warp CTA (64 registers): mask A instead (two LOPs per
+            // A word, shared by the two B rows) and keep B raw — 16 fewer live registers
+            uint4 bv[2][2];
 #pragma unroll
-            for (int c = 0; c < 2; ++c) {
-                bv[0][c] = load16_row<true>(pb + k0 + c * 64, 16, true);
-                bv[1][c] = load16_row<true>(pb + 8 * ldb + k0 + c * 64, 16, true);
-            }
+            for (int c = 0; c < 2; ++c)
 #pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                if (m >= M) break;  // uniform
+                for (int r = 0; r < 2; ++r) bv[r][c] = lb(r, c);
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    consume(bv, m, c, __ldg(reinterpret_cast<const uint4*>(pa + m * lda + k0 + c * 64)));
+            for (int mm = 0; mm < MW; ++mm) {
+                if (mb + mm >= M) break;  // uniform
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint4 av = la(mb + mm, c);
+                    const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
+#pragma unroll
+                    for (int r = 0; r < 2; ++r) {
+                        const uint32_t bw[4] = {bv[r][c].x, bv[r][c].y, bv[r][c].z, bv[r][c].w};
+                        int32_t sacc = acc[r * MW + mm];
+#pragma unroll
+                        for (int q = 0; q < 4; ++q)
+                            sacc = sat_word_add(aw[q] & 0x0000FFFFu, aw[q] & 0xFFFF0000u, bw[q], sacc);
+                        acc[r * MW + mm] = sacc;
+                    }
+                }
             }
         } else {
-            // ragged chunk (K tail, last row group, unaligned operands): bounded loads, zero fill
+        uint32_t blo[2][2][4], bhi[2][2][4];
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int r = 0; r < 2; ++r) {
+                const uint4 bv = lb(r, c);
+                const uint32_t w[4] = {bv.x, bv.y, bv.z, bv.w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    blo[r][c][q] = w[q] & 0x0000FFFFu;
+                    bhi[r][c][q] = w[q] & 0xFFFF0000u;
+                }
+            }
+        }
+#pragma unroll
+        for (int mm = 0; mm < MW; ++mm) {
+            if (mb + mm >= M) break;  // uniform
 #pragma unroll
             for (int c = 0; c < 2; ++c) {
-                const int64_t rem = kend - (k0 + c * 64 + t * 16);
-                bv[0][c] = load16_row<true>(pb + k0 + c * 64, (n0 + g < N) ? rem : 0, vec);
-                bv[1][c] = load16_row<true>(pb + 8 * ldb + k0 + c * 64, (n0 + g + 8 < N) ? rem : 0, vec);
-            }
+                const uint4 av = la(mb + mm, c);
+                const uint32_t aw[4] = {av.x, av.y, av.z, av.w};
 #pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                if (m >= M) break;
+                for (int r = 0; r < 2; ++r) {
+                    int32_t sacc = acc[r * MW + mm];
 #pragma unroll
-                for (int c = 0; c < 2; ++c)
-                    consume(bv, m, c, load16_row<false>(pa + m * lda + k0 + c * 64, kend - (k0 + c * 64 + t * 16), vec));
+                    for (int q = 0; q < 4; ++q) sacc = sat_pairs_add(aw[q], blo[r][c][q], bhi[r][c][q], sacc);
+                    acc[r * MW + mm] = sacc;
+                }
             }
+        }
+        }  // B-side masks
+    };
+#pragma unroll 1
+    for (int64_t ch = warp_k; ch < chunks && mb < M; ch += KS) {
+        const int64_t k0 = kbeg + ch * 128;  // k_range is a multiple of 128: pairs stay even-aligned
+        if ((vec_ok & 4) && rows_full && k0 + 128 <= kend) {
+            // whole chunk in range (warp-uniform): unconditional 16-byte loads (through L1 when
+            // sibling warps of other row groups read the same B bytes)
+            chunk(k0,
+                  [&](int r, int c) { return load16_row<MS == 1>(pb + r * 8 * ldb + k0 + c * 64, 16, true); },
+                  [&](int m, int c) { return __ldg(reinterpret_cast<const uint4*>(pa + m * lda + k0 + c * 64)); });
+        } else {
+            // ragged chunk (K tail, last row group, unaligned operands): bounded loads, zero fill
+            chunk(k0,
+                  [&](int r, int c) {
+                      return load16_row<MS == 1>(pb + r * 8 * ldb + k0 + c * 64,
+                                                 (n0 + g + 8 * r < N) ? kend - (k0 + c * 64 + t * 16) : 0, vec);
+                  },
+                  [&](int m, int c) {
+                      return load16_row<false>(pa + m * lda + k0 + c * 64, kend - (k0 + c * 64 + t * 16), vec);
+                  });
         }
     }
     // fold the quad's 4 K phases: after offsets 1 and 2 each lane holds V/4 totals
@@ -580,13 +639,13 @@ __global__ void __launch_bounds__(WARPS * 32)
                                           static_cast<uint32_t>(__shfl_xor_sync(0xffffffffu, acc[0], 2)));
         }
     }
-    // lane (g, t) now holds values base .. base + LEFT - 1 of the index space r * MT + m
+    // lane (g, t) now holds values base .. base + LEFT - 1 of the index space r * MW + mm
     constexpr int LEFT = V >= 4 ? V / 4 : 1;
     if (V >= 4 || (t & 2) == 0) {
 #pragma unroll
         for (int i = 0; i < LEFT; ++i) {
-            const int idx = base + i, r = idx / MT, m = idx - r * MT;
-            red[(warp * 16 + g + 8 * r) * MT + m] = acc[i];
+            const int idx = base + i, r = idx / MW, m = mb + idx - r * MW;
+            red[(warp_k * 16 + g + 8 * r) * MT + m] = acc[i];
         }
     }
     __syncthreads();
@@ -594,7 +653,7 @@ __global__ void __launch_bounds__(WARPS * 32)
         const int m = i / 16, row = i % 16;
         uint32_t s = 0;
 #pragma unroll
-        for (int w = 0; w < WARPS; ++w) s += static_cast<uint32_t>(red[(w * 16 + row) * MT + m]);
+        for (int w = 0; w < KS; ++w) s += static_cast<uint32_t>(red[(w * 16 + row) * MT + m]);
         const int64_t n = n0 + row;
         if (m < M && n < N) {
             int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;

@@ -586,7 +586,7 @@ ngemm_status launch_skinny_mma_t(const uint8_t* a, int64_t lda, const int8_t* b,
 // Saturating load-stream variant (skinny_sat_kernel): 16 B-rows per CTA, 8/16/32 warps split
 // the K range; the work is CUDA-core (ALU) bound for larger M, so a grid K split (atomic
 // wrap-add into a zeroed C) spreads it over every SM when there are few row groups.
-template <int MT, int WARPS>
+template <int MT, int WARPS, bool MSPLIT>
 ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
                                  int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, const DevInfo& di,
                                  cudaStream_t st, const Batch& bt) {
@@ -598,7 +598,7 @@ ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b,
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
-    NG_LAUNCH(skinny_sat_kernel<MT, WARPS>,
+    NG_LAUNCH(skinny_sat_kernel<MT, WARPS, MSPLIT>,
               dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
               dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
               splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
@@ -611,13 +611,27 @@ ngemm_status launch_skinny_sat_t(const uint8_t* a, int64_t lda, const int8_t* b,
                                  const Batch& bt = Batch()) {
     const int64_t groups = (n + 15) / 16 * bt.count;
     const int64_t chunks = (k + 127) / 128;
+    // Few 16-row groups x K chunks (< 4 warps per SM): split A's rows over warps too (MSPLIT),
+    // else one warp per K slice (profiles/r2/skinny_sat_r2.log)
+    if (MT > 4 && groups * chunks < 4 * static_cast<int64_t>(di.sms)) {
+        constexpr int MS = MT > 4 ? MT / 4 : 1;
+        const int64_t want = static_cast<int64_t>(di.sms) * 24;
+        const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + groups * MS - 1) / (groups * MS)));
+        int warps = ks * MS <= 8 ? 8 : 16;
+        if (opt(O_SKINNY_WARPS) > 0) warps = opt(O_SKINNY_WARPS);  // experiments: 8 / 16 / 32
+        const int64_t kw = warps / MS;
+        const int64_t splits = std::max<int64_t>(1, (ks + kw - 1) / kw);
+        if (warps >= 32) return launch_skinny_sat_w<MT, 32, true>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+        if (warps >= 16) return launch_skinny_sat_w<MT, 16, true>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+        return launch_skinny_sat_w<MT, 8, true>(a, lda, b, ldb, c, ldc, m, n, k, splits, di, st, bt);
+    }
     const int64_t want = static_cast<int64_t>(di.sms) * (MT >= 8 ? 16 : 32);  // resident warps to fill
     const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (want + groups - 1) / groups));
     constexpr int WMAX = MT >= 8 ? 16 : 32;  // 1024-thread CTAs cap registers at 64: spills for MT >= 8
-    if (ks <= 8) return launch_skinny_sat_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, 1, di, st, bt);
+    if (ks <= 8) return launch_skinny_sat_w<MT, 8, false>(a, lda, b, ldb, c, ldc, m, n, k, 1, di, st, bt);
     if (ks <= 16 || WMAX == 16)
-        return launch_skinny_sat_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 15) / 16, di, st, bt);
-    return launch_skinny_sat_w<MT, 32>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 31) / 32, di, st, bt);
+        return launch_skinny_sat_w<MT, 16, false>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 15) / 16, di, st, bt);
+    return launch_skinny_sat_w<MT, 32, false>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 31) / 32, di, st, bt);
 }
 
 // Lanes-own-rows variant (skinny_rows_kernel): 32-row tiles of B x K splits.
