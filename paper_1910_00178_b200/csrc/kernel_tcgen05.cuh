@@ -76,6 +76,22 @@ struct TileMap {
     int8_t* rq_out;
     int64_t rq_ldo;
     int rq_zp;
+    // Tail split: the first full_tiles tiles run whole; every later tile (the last, partial wave)
+    // runs as two half-width tiles (BN/2 columns each), so a wave that would leave more than half
+    // of the SMs idle becomes a wave of half-length work items on (nearly) all of them.
+    int full_tiles;
+    __device__ __forceinline__ int work_items(int num_tiles) const { return full_tiles + 2 * (num_tiles - full_tiles); }
+    // work item u -> tile coordinates and half (-1 = whole tile, 0 / 1 = left / right half)
+    __device__ __forceinline__ void item(int u, int& tm, int& tn, int& ks, int& half) const {
+        if (u < full_tiles) {
+            coords(u, tm, tn, ks);
+            half = -1;
+        } else {
+            const int v = u - full_tiles;
+            coords(full_tiles + (v >> 1), tm, tn, ks);
+            half = v & 1;
+        }
+    }
     __device__ __forceinline__ void coords(int t, int& tm, int& tn, int& ks) const {
         const int per_split = tiles_m * tiles_n;
         ks = t / per_split;
@@ -97,7 +113,7 @@ struct TileMap {
 template <int BN, int STAGES, int CG, int MC = 1>
 __global__ void __launch_bounds__(tc::THREADS, 1)
     tc_gemm_kernel(const __grid_constant__ CUtensorMap tma_a, const __grid_constant__ CUtensorMap tma_b,
-                   const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
+                   const __grid_constant__ CUtensorMap tma_b_half, const __grid_constant__ CUtensorMap tma_c, int32_t* __restrict__ C, int64_t ldc, int M, int N,
                    int num_kb_total, TileMap map, int c_mode) {
     // c_mode: 0 = TMA tensor store of C (SWIZZLE_128B staging), 1 = TMA reduce-add into a
     // zeroed C (split-K), 2 = direct scalar stores (C not TMA-describable), 3 = direct 16-byte
@@ -123,13 +139,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     const uint16_t pair_mask = static_cast<uint16_t>(((1u << CG) - 1u) << leader);
     const int unit = static_cast<int>(blockIdx.x) / CL;
     const int num_units = static_cast<int>(gridDim.x) / CL;
-    const int num_tiles = map.tiles_m * map.tiles_n * map.splits;
+    const int num_tiles = map.work_items(map.tiles_m * map.tiles_n * map.splits);  // work items
     const int kb_per_split = (num_kb_total + map.splits - 1) / map.splits;
 
     pdl_launch_dependents();
 
     // ---------------- TMA producer state (warp 0, one thread; both CTAs of a pair)
-    int p_t = unit, p_kb = 0, p_kb1 = 0, p_s = 0, p_row_a = 0, p_row_b = 0;
+    int p_t = unit, p_kb = 0, p_kb1 = 0, p_s = 0, p_row_a = 0, p_row_b = 0, p_half = -1;
     uint32_t p_ph = 0;
     bool p_open = false;
     auto produce = [&](int budget) {
@@ -141,14 +157,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         while (p_t < num_tiles && budget != 0) {
             if (!p_open) {
                 int tm, tn, ks;
-                map.coords(p_t, tm, tn, ks);
+                map.item(p_t, tm, tn, ks, p_half);
                 tn = tn * MC + static_cast<int>(pair);
                 p_kb = ks * kb_per_split;
                 p_kb1 = min(num_kb_total, p_kb + kb_per_split);
                 p_row_a = tm * UMMA_M + static_cast<int>(rank) * tc::BM;
-                p_row_b = tn * BN + static_cast<int>(rank) * (BN / CG);
+                p_row_b = p_half < 0 ? tn * BN + static_cast<int>(rank) * (BN / CG)
+                                     : tn * BN + p_half * (BN / 2) + static_cast<int>(rank) * (BN / (2 * CG));
                 p_open = true;
             }
+            const CUtensorMap* tb = p_half < 0 ? &tma_b : &tma_b_half;
+            const uint32_t stage_tx = S::A_BYTES + (p_half < 0 ? S::B_BYTES : S::B_BYTES / 2);
             if (p_kb >= p_kb1) {
                 p_t += num_units;
                 p_open = false;
@@ -160,7 +179,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             if (CG == 1 && (map.dbg & 4)) {
                 mbar_arrive(&full[p_s]);  // probes only: no operand traffic
             } else if constexpr (CG == 1) {
-                mbar_arrive_expect_tx(&full[p_s], S::STAGE_BYTES);
+                mbar_arrive_expect_tx(&full[p_s], MC == 1 ? stage_tx : S::STAGE_BYTES);
                 if constexpr (MC == 1) {
                     tma_load_2d(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
                 } else {
@@ -168,10 +187,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     tma_load_2d_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[p_s], p_kb * tc::BK,
                                    p_row_a + static_cast<int>(pair) * (tc::BM / 2), static_cast<uint16_t>(0x3), pol_a);
                 }
-                tma_load_2d(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
+                tma_load_2d(sb, tb, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
             } else {
                 // both CTAs' bytes land on the leader's full barrier; the leader arms it
-                if (rank == 0) mbar_arrive_expect_tx(&full[p_s], 2 * S::STAGE_BYTES);
+                if (rank == 0) mbar_arrive_expect_tx(&full[p_s], 2 * (MC == 1 ? stage_tx : S::STAGE_BYTES));
                 if constexpr (MC == 1) {
                     tma_load_2d_cg2(sa, &tma_a, &full[p_s], p_kb * tc::BK, p_row_a, pol_a);
                 } else {
@@ -180,7 +199,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     tma_load_2d_cg2_mc(sa + pair * (S::A_BYTES / 2), &tma_a, &full[p_s], p_kb * tc::BK,
                                        p_row_a + static_cast<int>(pair) * (tc::BM / 2), mask, pol_a);
                 }
-                tma_load_2d_cg2(sb, &tma_b, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
+                tma_load_2d_cg2(sb, tb, &full[p_s], p_kb * tc::BK, p_row_b, pol_b);
             }
             ++p_kb;
             if (++p_s == STAGES) { p_s = 0; p_ph ^= 1; }
@@ -191,8 +210,9 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tma_a);
         tma_prefetch(&tma_b);
+        if (map.full_tiles < map.tiles_m * map.tiles_n * map.splits) tma_prefetch(&tma_b_half);
         if (c_mode <= 1) tma_prefetch(&tma_c);
-        if (MC == 1 && map.prefetch && unit < num_tiles) {
+        if (MC == 1 && map.prefetch && unit < map.full_tiles) {
             // warm L2 with this CTA's first STAGES operand slabs before the dependency wait
             // (tma_prefetch_tile_2d: prefetch only, re-read after pdl_wait), so the first HBM
             // round trips overlap the preceding grid's tail and this CTA's setup
@@ -241,14 +261,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (single thread of the leader CTA)
-            const uint32_t idesc = idesc_i8(UMMA_M, BN, map.a_signed != 0, map.b_signed != 0);
+            const uint32_t idesc_full = idesc_i8(UMMA_M, BN, map.a_signed != 0, map.b_signed != 0);
+            const uint32_t idesc_half = idesc_i8(UMMA_M, BN / 2, map.a_signed != 0, map.b_signed != 0);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
             uint32_t acc_ph = 0;
             for (int t = unit; t < num_tiles; t += num_units) {
-                int tm, tn, ks;
-                map.coords(t, tm, tn, ks);
+                int tm, tn, ks, half;
+                map.item(t, tm, tn, ks, half);
+                const uint32_t idesc = half < 0 ? idesc_full : idesc_half;
                 const int kb0 = ks * kb_per_split;
                 const int kb1 = min(num_kb_total, kb0 + kb_per_split);
                 mbar_wait(&tempty[acc], acc_ph ^ 1);
@@ -288,9 +310,11 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
         int acc = 0, cbuf = 0;
         uint32_t acc_ph = 0;
         for (int t = unit; t < num_tiles; t += num_units) {
-            int tm, tn, ks;
-            map.coords(t, tm, tn, ks);
+            int tm, tn, ks, half;
+            map.item(t, tm, tn, ks, half);
             tn = tn * MC + static_cast<int>(pair);
+            const int ncols = half < 0 ? BN : BN / 2;
+            const int col_base = tn * BN + (half < 0 ? 0 : half * (BN / 2));
             const int kb0 = ks * kb_per_split;
             const bool has_k = kb0 < num_kb_total;
             mbar_wait(&tfull[acc], acc_ph);
@@ -299,7 +323,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             const int row0 = tm * UMMA_M + static_cast<int>(rank) * tc::BM + ew * 32;
             const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
 #pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
+            for (int c = 0; c < ncols; c += 32) {
                 uint32_t v[32];
                 tmem_ld_32x32b_x32(taddr + c, v);
                 tmem_wait_ld();
@@ -309,7 +333,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] <<= map.shift;  // mod 2^32, like the accumulator
                 }
-                const int col0 = tn * BN + c;
+                const int col0 = col_base + c;
                 if (c_mode == 4) {
                     // fused requantisation to int8: each lane loads one column's scale / bias and
                     // the warp broadcasts them; lane = row, 32 int8 per row, two 16-byte stores

@@ -812,7 +812,7 @@ struct TcOps {
 };
 
 template <int BN, int STAGES, int CG, int MC = 1>
-ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tcmap, int32_t* c,
+ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUtensorMap& tbh, const CUtensorMap& tcmap, int32_t* c,
                          int64_t ldc, int64_t m, int64_t n, int64_t k, int splits, int c_mode, const DevInfo& di,
                          cudaStream_t st, const TcOps& ops) {
     using S = tc::Smem<BN, STAGES, CG>;
@@ -863,9 +863,17 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
         ngemm_status zs = zero_c(c, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
-    const int grid = std::min(tiles * map.splits, units) * CG * MC;
-    NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG * MC, 1, ta, tb, tcmap, c, ldc, static_cast<int>(m),
-              static_cast<int>(n), num_kb, map, c_mode);
+    // tail split (TileMap::full_tiles; TC_SCHED=1): a last wave less than half full runs as
+    // half-width tiles.  Bit-exact, but measured neutral (4096^3 55.6 vs 55.7 us, c5 within noise,
+    // profiles/r2/ab_tail_split_r2.log): the main waves are bound by L2->SM operand delivery, not
+    // by per-SM MMA time, so the idle SMs of a short last wave cost little.  Off by default.
+    map.full_tiles = tiles * map.splits;
+    const int rem = tiles % units;
+    if (MC == 1 && map.splits == 1 && rem > 0 && 2 * rem <= units && opt(O_TC_SCHED) == 1) map.full_tiles = tiles - rem;
+    const int work = map.full_tiles + 2 * (tiles * map.splits - map.full_tiles);
+    const int grid = std::min(work, units) * CG * MC;
+    NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG * MC, 1, ta, tb, tbh, tcmap, c, ldc,
+              static_cast<int>(m), static_cast<int>(n), num_kb, map, c_mode);
     return NGEMM_OK;
 }
 
@@ -889,23 +897,24 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
     }
     const TcPlan plan = plan_tcgen05(m, n, k, di.sms, c_tma ? 1 : 0);
     const TcCfgInfo& ci = kTcCfg[plan.cfg];
-    CUtensorMap ta, tb, tcm;
+    CUtensorMap ta, tb, tbh, tcm;
     std::memset(&tcm, 0, sizeof tcm);
     ngemm_status s = make_tmap_u8(&ta, a_use, k, m, lda_use, tc::BK, tc::BM / ci.mc);
     if (s == NGEMM_OK) s = make_tmap_u8(&tb, b_use, k, n, ldb_use, tc::BK, ci.bn / ci.cg);
+    if (s == NGEMM_OK) s = make_tmap_u8(&tbh, b_use, k, n, ldb_use, tc::BK, ci.bn / (2 * ci.cg));  // tail half tiles
     if (s == NGEMM_OK && c_tma) s = make_tmap_c(&tcm, c, m, n, ldc);
     const int c_mode = c_tma ? 0 : 2;
     if (s == NGEMM_OK) {
         switch (plan.cfg) {
-        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_MC128: s = launch_tc_t<128, 6, 1, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        case TC_MC64: s = launch_tc_t<64, 8, 1, 2>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
-        default: s = launch_tc_t<64, 8, 1>(ta, tb, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_PAIR256: s = launch_tc_t<256, 6, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_1CTA256: s = launch_tc_t<256, 4, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_1CTA128: s = launch_tc_t<128, 6, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_QUAD256: s = launch_tc_t<256, 6, 2, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_LEAN128: s = launch_tc_t<128, 2, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_MC128: s = launch_tc_t<128, 6, 1, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_MC64: s = launch_tc_t<64, 8, 1, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        default: s = launch_tc_t<64, 8, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         }
     }
     if (scratch) cudaFreeAsync(scratch, st);

@@ -378,6 +378,37 @@ def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, knobs):
             assert (got == oracle.gemm(a, b, EXACT)).all(), (cfg, splits, direct, m, n, k, ldc)
 
 
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3])
+def test_tcgen05_tail_split(cuda, oracle, cfg, knobs):
+    """Tail split (TileMap::full_tiles): when the last wave of tiles would leave more than half the
+    SMs idle, its tiles run as two half-width work items (N = BN/2 MMAs, half-height B boxes, half
+    the epilogue).  Shapes whose tile counts trigger it for every tile configuration, ragged ones
+    included (a half tile straddling N), bit-exact against the oracle, and the same with the split
+    switched off; plus the fused-requant epilogue on a split shape."""
+    import torch
+    knobs.set("TC_CFG", cfg)
+    shapes = [(4096, 1280, 640), (4000, 1250, 333), (2048, 2560, 384), (1000, 9000, 256)]
+    for (m, n, k) in shapes:
+        a = oracle.mat_random_u8(m, k, m + 7)
+        b = oracle.mat_random_i8(n, k, n + 7)
+        ref = oracle.gemm(a, b, EXACT)
+        for sched in (1, 0):
+            knobs.set("TC_SCHED", sched)
+            got = dev_gemm(a, b, EXACT, "tcgen05")
+            assert (got == ref).all(), (cfg, sched, m, n, k, int((got != ref).sum()))
+    knobs.set("TC_SCHED", 1)
+    m, n, k = 4096, 1280, 640
+    a = oracle.mat_random_u8(m, k, 3)
+    b = oracle.mat_random_i8(n, k, 4)
+    scale = np.linspace(1e-4, 3e-3, n).astype(np.float32)
+    bias = np.arange(n, dtype=np.int32) * 37 - 20000
+    out = api.gemm_device_requant(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                                  torch.from_numpy(scale).cuda(), torch.from_numpy(bias).cuda(), zero_point=3)
+    torch.cuda.synchronize()
+    y = requant_ref(oracle.gemm(a, b, EXACT), scale, bias, 3)
+    assert (out.cpu().numpy() == y).all(), int((out.cpu().numpy() != y).sum())
+
+
 @pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
 def test_skinny_variants(cuda, oracle, golden, variant, knobs):
     """Skinny (M <= 16) variants: 0 warp-butterfly dp4a, 1 lanes-own-rows dp4a (broadcast A),
