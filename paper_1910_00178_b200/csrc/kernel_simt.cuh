@@ -14,8 +14,10 @@
 // K staged through shared memory 32 bytes (8 words) at a time, transposed to word-major so the
 // inner loop is LDS.128 per 4 operand words; next-stage global loads are prefetched into
 // registers.  Small problems add K splits (atomic wrap-add into a zeroed C) to fill 148 SMs.
-// The saturating inner step is 2 IDP.4A + 4 VIMNMX + 1 IADD3 per 4 MACs — CUDA-core (ALU
-// pipe) bound, which is why inputs that provably cannot saturate go to the tensor cores.
+// The saturating inner step (sat_word_add, ptx.cuh) is 2 IDP.4A on the masked A halves, one
+// I2IP.S16.S32.SAT packing both pair sums with int16 saturation and one IDP.2A wrap-adding
+// them: 4 instructions per 4 MACs, CUDA-core (IDP pipe) bound — which is why the pairs that
+// provably cannot saturate go to the tensor cores for large shapes (kernel_satfix.cuh).
 #pragma once
 
 #include "ptx.cuh"
