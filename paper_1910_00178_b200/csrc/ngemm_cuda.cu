@@ -774,7 +774,9 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
             const double kb = static_cast<double>((num_kb + splits - 1) / splits);
             double t = static_cast<double>(waves) * kb * ci.cycles_per_kb + 600.0 + ci.bn * 8.0;
             if (splits > 1) t += 1500.0;                 // zeroing C + reduce-add traffic
-            if (ci.cg == 2) t *= 0.97;                    // less L2->SM traffic per MAC
+            // pairs: less L2->SM traffic per MAC, but ~1000 cycles more fixed cost (cluster launch
+            // and sync) — 2048^3: 128x256 1-CTA tiles 11.7 us vs pairs 12.9 (profiles/r2/ab_tc_cfg_r2.log)
+            if (ci.cg == 2) t = t * 0.97 + 1000.0;
             if (ci.mc == 2) t *= 0.98;                    // A multicast: a further 25% less
             if (t < best_t) {
                 best_t = t;
