@@ -833,7 +833,11 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     const int units = di.sms / (CG * MC);
     // split-K needs the TMA reduce-add epilogue (C must be TMA-describable)
     map.splits = c_mode == 2 ? 1 : std::max(1, std::min(splits, num_kb));
-    map.group_m = tc::GROUP_M;
+    // raster group: as many M tiles as keep the group's A rows (group_m x 128*CG rows x K bytes)
+    // within ~32 MiB of L2 — 16384^3: 8 (pairs), 8192^3: 16, K <= 4096: every M tile
+    // (profiles/r2/ab_groupm_hint_r2.log: 8192^3 363 -> 356 us, 4096^3 55.6 -> 54.3 us, c5 unchanged)
+    map.group_m = static_cast<int>(std::max<int64_t>(
+        1, std::min<int64_t>(map.tiles_m, (int64_t(32) << 20) / (static_cast<int64_t>(tc::BM) * CG * std::max<int64_t>(k, 1)))));
     // pre-issuing the first loads before the block sync measured slower (profiles/ab_preissue_r1.log)
     map.preissue = opt(O_TC_PREISSUE);  // experiments
     map.l2hint = opt(O_TC_L2HINT);      // experiments (default 7: A evict_last, B and C evict_first; profiles/r2/l2hint_r2.log)
