@@ -75,8 +75,9 @@ public:
 private:
     CopyPool() {
         const unsigned hw = std::thread::hardware_concurrency();
-        // measured on the 16-thread GPU host (profiles/r2/e2e_probe.log): 8 copying threads beat 4 and 16
-        nthreads_ = static_cast<int>(std::max(2u, std::min(7u, hw > 2 ? hw / 2 : 2u)));
+        // measured on the 16-thread GPU host (profiles/r2/e2e_probe.log): 12 copying threads (11
+        // workers + the caller) with 8 staging slots per direction beat 8 and 16
+        nthreads_ = static_cast<int>(std::max(2u, std::min(15u, hw >= 4 ? hw * 3 / 4 - 1 : 2u)));
         if (const char* e = std::getenv("NGEMM_COPY_THREADS")) nthreads_ = std::max(1, std::atoi(e));  // experiments
         for (int i = 0; i < nthreads_; ++i)
             std::thread([this] {
@@ -280,8 +281,12 @@ ngemm_status host_pipeline(const HostGemm& g) {
     ck(cudaStreamCreateWithFlags(&sout, cudaStreamNonBlocking), "stream");
     for (auto& e : ev) ck(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     std::vector<Slot> in_slots, out_slots;
-    if (s == NGEMM_OK && stage_in && !take_slots(4, in_slots)) s = fail(NGEMM_ERR_CUDA, "pinned staging allocation failed");
-    if (s == NGEMM_OK && stage_out && !take_slots(4, out_slots)) s = fail(NGEMM_ERR_CUDA, "pinned staging allocation failed");
+    static const int nslots = [] {  // experiments: NGEMM_STAGE_SLOTS (read once)
+        const char* e = std::getenv("NGEMM_STAGE_SLOTS");
+        return e ? std::max(2, std::atoi(e)) : 8;
+    }();
+    if (s == NGEMM_OK && stage_in && !take_slots(nslots, in_slots)) s = fail(NGEMM_ERR_CUDA, "pinned staging allocation failed");
+    if (s == NGEMM_OK && stage_out && !take_slots(nslots, out_slots)) s = fail(NGEMM_ERR_CUDA, "pinned staging allocation failed");
     uint8_t* buf = nullptr;
     if (s == NGEMM_OK) ck(dev_alloc(&buf, c_off + c_bytes, sin), "device allocation");
     int32_t* dc = buf ? reinterpret_cast<int32_t*>(buf + c_off) : nullptr;
