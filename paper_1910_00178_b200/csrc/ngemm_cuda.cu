@@ -830,7 +830,38 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     map.tiles_n = static_cast<int>((n + BN - 1) / BN) / MC;  // MC adjacent N tiles per cluster
     const int num_kb = static_cast<int>((k + tc::BK - 1) / tc::BK);
     const int tiles = map.tiles_m * map.tiles_n;
-    const int units = di.sms / (CG * MC);
+    // persistent units = clusters that can be resident at once: a cluster must fit in one GPC,
+    // so with 4-CTA clusters (or 2-CTA ones on GPCs with an odd SM count) fewer than
+    // SMs / cluster size are co-resident, and a grid sized SMs / cluster size would run its last
+    // clusters as a second wave after the others finish
+    static std::atomic<int> max_clusters[64] = {};
+    int units = di.sms / (CG * MC);
+    if (CG * MC > 1) {
+        std::atomic<int>& mc = max_clusters[dev & 63];
+        if (mc.load() == 0) {
+            cudaLaunchConfig_t cfg = {};
+            cfg.gridDim = dim3(static_cast<unsigned>(units * CG * MC));
+            cfg.blockDim = dim3(tc::THREADS);
+            cfg.dynamicSmemBytes = S::TOTAL;
+            cudaLaunchAttribute attr;
+            attr.id = cudaLaunchAttributeClusterDimension;
+            attr.val.clusterDim.x = CG * MC;
+            attr.val.clusterDim.y = 1;
+            attr.val.clusterDim.z = 1;
+            cfg.attrs = &attr;
+            cfg.numAttrs = 1;
+            int n_active = 0;
+            if (cudaOccupancyMaxActiveClusters(&n_active, kern, &cfg) != cudaSuccess || n_active <= 0) {
+                cudaGetLastError();
+                n_active = units;
+            }
+            mc.store(n_active);
+            if (std::getenv("NGEMM_VERBOSE"))
+                std::fprintf(stderr, "ngemm: tc_gemm_kernel<%d,%d,%d,%d>: %d co-resident clusters of %d CTAs\n", BN,
+                             STAGES, CG, MC, n_active, CG * MC);
+        }
+        units = std::min(units, mc.load());
+    }
     // split-K needs the TMA reduce-add epilogue (C must be TMA-describable)
     map.splits = c_mode == 2 ? 1 : std::max(1, std::min(splits, num_kb));
     // raster group: as many M tiles as keep the group's A rows (group_m x 128*CG rows x K bytes)
