@@ -164,3 +164,33 @@ def test_tune_store_round_trip_and_malformed(tmp_path):
     with pytest.raises(api.ConfigError):
         api.tune_store_load(str(bad))
     api.tune_clear()
+
+
+def test_option_table_read_once_and_settable():
+    """Experiment knobs: read once from NGEMM_<NAME> (never on the launch path), changed through
+    the C-ABI, unknown names rejected with ConfigError, reset re-reads the environment."""
+    import subprocess
+    import sys
+    code = (
+        "import sys; sys.path.insert(0, %r)\n"
+        "from paper_1910_00178_b200 import _lib\n"
+        "assert _lib.get_option('TC_CFG') == 3, _lib.get_option('TC_CFG')\n"
+        "assert _lib.get_option('NGEMM_TC_CFG') == 3\n"
+        "assert _lib.get_option('I16_PATH') == 1\n"
+        "assert _lib.get_option('TC_L2HINT') == 7\n"
+        "_lib.set_option('TC_CFG', 5); assert _lib.get_option('TC_CFG') == 5\n"
+        "with _lib.options(TC_SPLITS=2):\n"
+        "    assert _lib.get_option('TC_SPLITS') == 2\n"
+        "assert _lib.get_option('TC_SPLITS') == -1\n"
+        "_lib.reset_options(); assert _lib.get_option('TC_CFG') == 3\n"
+        "assert _lib.get_option('NO_SUCH_KNOB') == -2**31\n"
+        "try:\n"
+        "    _lib.set_option('NO_SUCH_KNOB', 1)\n"
+        "    raise SystemExit('accepted an unknown option')\n"
+        "except _lib.ConfigError:\n"
+        "    pass\n"
+        "print('ok')\n") % ROOT
+    env = dict(os.environ, NGEMM_TC_CFG="3", NGEMM_I16_PATH="tcgen05")
+    env.pop("NGEMM_TC_L2HINT", None)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=120)
+    assert r.returncode == 0 and r.stdout.strip() == "ok", r.stdout + r.stderr
