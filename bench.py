@@ -593,16 +593,17 @@ def run_ours(args):
 
     # verification of the timed output (reference bench discipline: nothing unverified is timed)
     verified = None
-    if not args.no_verify and mr > 0:
-        bad, checked = verify_rows(cs[0], a_full, b_host, mode, r0, rows=32 if mr * N * K > 1e11 else 128, blocks=3)
-        fr = freivalds(cs[0], as_[0], bs[0]) if mode == EXACT else None
-        ok_local = 1.0 if (bad == 0 and fr is not False) else 0.0
-        ok = min_over_ranks(ok_local, world) == 1.0
-        verified = ok
+    verify_desc = "skipped"
+    if not args.no_verify:  # every rank joins the agreement, even one without rows
+        ok_local, checked = 1.0, 0
+        if mr > 0:
+            bad, checked = verify_rows(cs[0], a_full, b_host, mode, r0, rows=32 if mr * N * K > 1e11 else 128,
+                                       blocks=3)
+            fr = freivalds(cs[0], as_[0], bs[0]) if mode == EXACT else None
+            ok_local = 1.0 if (bad == 0 and fr is not False) else 0.0
+        verified = min_over_ranks(ok_local, world) == 1.0
         verify_desc = (f"rank {rank}: {checked} rows (first/middle/last blocks) bit-exact vs the CPU oracle" +
                        ("; 8 Freivalds rounds (x in [0,16), float64) over the whole C" if mode == EXACT else ""))
-    else:
-        verify_desc = "skipped"
 
     # sustained: 300 back-to-back steps (the int8 GEMM at full rate is power-capped on this part)
     sustained = None
@@ -718,7 +719,7 @@ def run_e2e(args, world, mr, N, K, mode, kernel, a_host, b_host, a_dev, total_op
         if mr > 0:
             _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_p.data_ptr(), b_p.data_ptr(), c_p.data_ptr(), mr, N, K, mode,
                                                    kernel))
-    out = rec(timed(pinned), mr * K + N * K, 4 * mr * N,
+    out = rec(timed(pinned), (mr * K + N * K) if mr > 0 else 0, 4 * mr * N,
               "ngemm_cuda_gemm_u8i8_host (C-ABI, pinned host A/B/C, synchronous per call)")
     variants = {}
     c_np = np.empty((max(mr, 1), N), np.int32)
@@ -727,23 +728,24 @@ def run_e2e(args, world, mr, N, K, mode, kernel, a_host, b_host, a_dev, total_op
         if mr > 0:
             _lib.check(L.ngemm_cuda_gemm_u8i8_host(a_host.ctypes.data, b_host.ctypes.data, c_np.ctypes.data, mr, N, K,
                                                    mode, kernel))
-    variants["pageable"] = rec(timed(pageable), mr * K + N * K, 4 * mr * N,
+    variants["pageable"] = rec(timed(pageable), (mr * K + N * K) if mr > 0 else 0, 4 * mr * N,
                                "ngemm_cuda_gemm_u8i8_host on pageable host memory (gemm_conventional on MatrixBufs)")
+    # every rank runs the same collectives (timed() and rec() reduce over ranks), rows or not
+    import ctypes as C
+    h = C.c_void_p()
     if mr > 0:
-        import ctypes as C
-        h = C.c_void_p()
         _lib.check(L.ngemm_cuda_packed_from_device(a_dev.data_ptr(), a_dev.stride(0), mr, K, C.byref(h)))
 
-        def resident():
+    def resident():
+        if mr > 0:
             _lib.check(L.ngemm_cuda_gemm_packed_resident_host(h, b_p.data_ptr(), c_p.data_ptr(), N, mode))
-        try:
-            variants["resident_weight"] = rec(timed(resident), N * K, 4 * mr * N,
-                                              "ngemm_cuda_gemm_packed_resident_host (gemm_ngemm: weight A resident "
-                                              "in HBM; pinned B in, pinned C out per call)")
-        finally:
+    try:
+        variants["resident_weight"] = rec(timed(resident), N * K if mr > 0 else 0, 4 * mr * N,
+                                          "ngemm_cuda_gemm_packed_resident_host (gemm_ngemm: weight A resident "
+                                          "in HBM; pinned B in, pinned C out per call)")
+    finally:
+        if mr > 0:
             L.ngemm_cuda_packed_free(h)
-    else:
-        timed(lambda: None)
     if mr > 0:  # the pinned call's C must be the device result
         ok = bool(np.array_equal(c_p[:64].numpy(), c_np[:64]))
         out["checked"] = ok

@@ -315,9 +315,17 @@ ngemm_status host_pipeline(const HostGemm& g) {
     std::condition_variable tcv;
     int tiles_issued = 0;  // tile events recorded so far (by the issuing thread)
     bool abort_out = false;
+    // the drain thread keeps its own status (the library's error message is thread-local, and the
+    // issuing thread reads `s` without a lock); it is merged after the join
+    std::atomic<bool> out_failed{false};
+    std::string out_msg;
     std::thread out_thread;
     if (stage_out && s == NGEMM_OK) {
         out_thread = std::thread([&] {
+            auto ck = [&](cudaError_t e, const char* what) {
+                if (e != cudaSuccess && !out_failed.exchange(true)) out_msg = std::string(what) + ": " + cudaGetErrorString(e);
+                return e == cudaSuccess;
+            };
             struct Pending {
                 Slot* sl;
                 int64_t r0, c0, nr, nc;
@@ -336,6 +344,7 @@ ngemm_status host_pipeline(const HostGemm& g) {
                     {
                         std::unique_lock<std::mutex> lk(tmu);
                         tcv.wait(lk, [&] { return tiles_issued > t || abort_out; });
+                        if (out_failed.load()) abort_out = true;
                         if (abort_out && tiles_issued <= t) {
                             while (!q.empty()) q.pop_front();
                             return;
@@ -424,6 +433,7 @@ ngemm_status host_pipeline(const HostGemm& g) {
     }
     tcv.notify_all();
     if (out_thread.joinable()) out_thread.join();
+    if (out_failed.load() && s == NGEMM_OK) s = fail(NGEMM_ERR_CUDA, out_msg);
     if (buf) {
         cudaEvent_t ev_done = ev.back();
         ck(cudaEventRecord(ev_done, sout), "record");
