@@ -360,7 +360,10 @@ ngemm_status launch_simt_bytes(const uint8_t* a, int64_t lda, const int8_t* b, i
         return NGEMM_OK;
     }
     const int64_t tiles64 = ((m + 63) / 64) * ((n + 63) / 64);
-    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((target + tiles64 - 1) / tiles64, kbytes / 512));
+    // K splits down to 128 bytes until ~8 CTAs per SM: few-tile shapes were latency bound
+    // (128x1024x1024 sat 19.3 -> 12.2 us, others unchanged; profiles/r2/simt_split_r2.log)
+    const int64_t tgt = 8 * static_cast<int64_t>(di.sms);
+    int64_t splits = std::max<int64_t>(1, std::min<int64_t>((tgt + tiles64 - 1) / tiles64, kbytes / 128));
     const int64_t k_split = round_up((kbytes + splits - 1) / splits, 32);
     splits = (kbytes + k_split - 1) / k_split;
     if (splits > 1) {
