@@ -90,14 +90,17 @@ def load():
         L.ngemm_cuda_tune_store_save.argtypes = [C.c_char_p]
         L.ngemm_cuda_tune_store_load.argtypes = [C.c_char_p, C.POINTER(i32)]
         L.ngemm_cuda_tune_clear.argtypes = []
-        L.ngemm_cuda_set_option.argtypes = [C.c_char_p, i32]
-        L.ngemm_cuda_get_option.argtypes = [C.c_char_p]
-        L.ngemm_cuda_reset_options.argtypes = []
-        L.ngemm_cuda_trim.argtypes = []
-        L.ngemm_cuda_packed_upload_sharded.argtypes = [C.POINTER(PackedMeta), vp, C.c_size_t, C.POINTER(i32), i32,
-                                                       C.POINTER(vp)]
-        L.ngemm_cuda_gemm_packed_multi.argtypes = [C.POINTER(vp), i32, vp, vp, i64, i32]
+        if hasattr(L, "ngemm_cuda_set_option"):  # absent only in older builds loaded for A/B runs
+            L.ngemm_cuda_set_option.argtypes = [C.c_char_p, i32]
+            L.ngemm_cuda_get_option.argtypes = [C.c_char_p]
+            L.ngemm_cuda_reset_options.argtypes = []
+            L.ngemm_cuda_trim.argtypes = []
+            L.ngemm_cuda_packed_upload_sharded.argtypes = [C.POINTER(PackedMeta), vp, C.c_size_t, C.POINTER(i32), i32,
+                                                           C.POINTER(vp)]
+            L.ngemm_cuda_gemm_packed_multi.argtypes = [C.POINTER(vp), i32, vp, vp, i64, i32]
         for f in EXPORTS:
+            if os.environ.get("NGEMM_LIB") and not hasattr(L, f):
+                continue  # A/B against an older build (experiments only)
             fn = getattr(L, f)
             if f not in ("ngemm_cuda_abi_version", "ngemm_cuda_status_name", "ngemm_cuda_last_error",
                          "ngemm_cuda_pick_kernel", "ngemm_cuda_launch_count", "ngemm_cuda_get_option"):
@@ -109,7 +112,8 @@ def load():
         L.ngemm_cuda_pick_kernel.argtypes = [i64, i64, i64, i32]
         L.ngemm_cuda_pick_kernel.restype = C.c_int
         L.ngemm_cuda_launch_count.restype = C.c_uint64
-        L.ngemm_cuda_get_option.restype = C.c_int
+        if hasattr(L, "ngemm_cuda_get_option"):
+            L.ngemm_cuda_get_option.restype = C.c_int
         _lib = L
         return L
 

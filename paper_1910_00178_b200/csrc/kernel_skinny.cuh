@@ -470,8 +470,12 @@ namespace ngemm_dev {
 // shuffle levels (transposing, so each lane keeps 1/4 of the values), the CTA's warps meet in
 // shared memory.
 // ---------------------------------------------------------------------------------------------
-template <int MT, int WARPS, bool MSPLIT>
-__global__ void __launch_bounds__(WARPS * 32)
+// Register caps for the 8-warp CTAs: the B-mask form at <= 128 so two CTAs fit per SM (at 133
+// registers one CTA per SM made 16x4096x1024 13.1 us instead of 7.9), the A-mask form at <= 85
+// so three fit, <= 64 for MT <= 4 so four fit (batches are occupancy-bound: 95 registers / two
+// CTAs cost 26 % at 16x4096x1024 x 128; profiles/r2/batched_ab_r2.log)
+template <int MT, int WARPS, bool MSPLIT, bool BMASK>
+__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? (BMASK ? 2 : (MT <= 4 ? 4 : 3)) : 1)
     skinny_sat_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
                       int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range, int vec_ok,
                       int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc) {
@@ -534,9 +538,11 @@ __global__ void __launch_bounds__(WARPS * 32)
     // one chunk: B words (2 rows x 2 halves x 4 words) masked once, then every A row against them;
     // `lb` / `la` load 16 bytes of B / A (unconditional on the fast path, bounded on the ragged one)
     auto chunk = [&](int64_t k0, auto lb, auto la) {
-        if constexpr (MT == 1 || (MT <= 4 && WARPS >= 32)) {
-            // one A row, or few rows in a 32-warp CTA (64 registers): mask A instead (two LOPs per
-            // A word, shared by the two B rows) and keep B raw — 16 fewer live registers
+        if constexpr (!BMASK) {
+            // mask A instead (two LOPs per A word, shared by the two B rows) and keep B raw: 16
+            // fewer live registers — for one A row, 32-warp CTAs (64 registers), and batches, whose
+            // throughput depends on occupancy more than on the instruction count
+            // (profiles/r2/batched_ab_r2.log: 123 vs 80 registers cost 26 % at 16x4096x1024 x 128)
             uint4 bv[2][2];
 #pragma unroll
             for (int c = 0; c < 2; ++c)

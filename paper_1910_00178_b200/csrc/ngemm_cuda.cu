@@ -601,10 +601,19 @@ ngemm_status launch_skinny_sat_w(const uint8_t* a, int64_t lda, const int8_t* b,
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
-    NG_LAUNCH(skinny_sat_kernel<MT, WARPS, MSPLIT>,
-              dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
-              dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
-              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
+    // B-side pair masks (fewer instructions, more registers) for single latency-bound GEMMs;
+    // A-side masks for one A row, 64-register CTAs and batches (occupancy-bound)
+    constexpr bool bmask_ok = MT > 1 && !(MT <= 4 && WARPS >= 32);
+    if (bmask_ok && bt.count == 1)
+        NG_LAUNCH(skinny_sat_kernel<MT, WARPS, MSPLIT, bmask_ok>,
+                  dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
+                  dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
+                  splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
+    else
+        NG_LAUNCH(skinny_sat_kernel<MT, WARPS, MSPLIT, false>,
+                  dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
+                  dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
+                  splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
     return NGEMM_OK;
 }
 
