@@ -193,12 +193,14 @@ __device__ __forceinline__ int32_t sat2_add(int32_t p0, int32_t p1, int32_t acc)
 __global__ void __launch_bounds__(satfix::THREADS, 1)
     sat_fix_kernel(const __grid_constant__ CUtensorMap tma_c, const uint32_t* __restrict__ apm,
                    const uint8_t* __restrict__ bt, const uint8_t* __restrict__ lt, const uint32_t* __restrict__ flags,
-                   int64_t chunks, int64_t chunks_per_split, const int32_t* __restrict__ guard) {
+                   int64_t chunks, int64_t tiles_n, int64_t total_units, int64_t total_pairs,
+                   const int32_t* __restrict__ guard) {
     using namespace satfix;
     // no early launch_dependents: the next grid's CTAs would wait in SM slots this grid still
     // needs; they launch as this grid's CTAs exit
     pdl_wait();
-    if (*reinterpret_cast<const volatile unsigned long long*>(guard + 4) == 0) return;  // nothing can clamp
+    const unsigned long long listed = *reinterpret_cast<const volatile unsigned long long*>(guard + 4);
+    if (listed == 0) return;  // nothing can clamp
     extern __shared__ uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1024-aligned
     uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * STAGE);
@@ -206,159 +208,184 @@ __global__ void __launch_bounds__(satfix::THREADS, 1)
     int* list = reinterpret_cast<int*>(smem + 2 * STAGE + 64);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int64_t t = blockIdx.x, u = blockIdx.y;
-    const int64_t c_begin = static_cast<int64_t>(blockIdx.z) * chunks_per_split;
-    const int64_t c_end = min(chunks, c_begin + chunks_per_split);
-    if (warp == 0) {  // the chunks with dangerous pairs, compacted by ballots
-        int cnt = 0;
-        for (int64_t cb = c_begin; cb < c_end; cb += 32) {
-            const int64_t c = cb + lane;
-            const bool hit = c < c_end && flags[t * chunks + c] != 0u;
-            const uint32_t bal = __ballot_sync(0xffffffffu, hit);
-            if (hit) list[cnt + __popc(bal & ((1u << lane) - 1u))] = static_cast<int>(c);
-            cnt += __popc(bal);
-        }
-        if (lane == 0) {
-            *nlist_p = cnt;
-            mbar_init(&full[0], 1);
-            mbar_init(&full[1], 1);
-            fence_mbar_init();
-        }
+    if (tid == 0) {
+        mbar_init(&full[0], 1);
+        mbar_init(&full[1], 1);
+        fence_mbar_init();
     }
-    __syncthreads();
-    const int nl_count = *nlist_p;
-    if (nl_count == 0) return;  // block-uniform: no dangerous pair in this tile's K range
-
-    auto issue = [&](int i) {
-        const int s = i & 1;
-        const int64_t c = list[i];
-        uint8_t* st = smem + s * STAGE;
-        mbar_arrive_expect_tx(&full[s], STAGE);
-        bulk_load_1d(st, apm + (u * chunks + c) * (A_TILE / 4), A_TILE, &full[s]);
-        bulk_load_1d(st + A_TILE, bt + (t * chunks + c) * B_TILE, B_TILE, &full[s]);
-        bulk_load_1d(st + A_TILE + B_TILE, lt + (t * chunks + c) * L_TILE, L_TILE, &full[s]);
-    };
-    if (tid == 0) issue(0);
-
-    int32_t acc[NPW][8];  // [row of B][t]: A row l + 32 t
-#pragma unroll
-    for (int i = 0; i < NPW; ++i)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) acc[i][e] = 0;
-
-    for (int i = 0; i < nl_count; ++i) {
-        // the other stage was released by the __syncthreads that ended iteration i - 1
-        if (tid == 0 && i + 1 < nl_count) issue(i + 1);
-        mbar_wait(&full[i & 1], (i >> 1) & 1);
-        // shared-window addresses: the loads below are plain LDS
-        const uint32_t st = smem_u32(smem) + (i & 1) * STAGE;
-        const uint32_t sa = st + lane * 16;             // + j * 512: pair j of this lane's 8 rows
-        const uint32_t sc = st + A_TILE + B_TILE;       // counts, then the index lists
-        // all 8 of this warp's rows fully listed (extreme inputs): pair-major loop, each pair of A
-        // words loaded once for the 8 rows instead of once per row
-        const uint32_t c_lo = lds_u32(sc + warp * NPW), c_hi = lds_u32(sc + warp * NPW + 4);
-        if (c_lo == 0x80808080u && c_hi == 0x80808080u) {
-            const uint32_t sb0 = st + A_TILE + warp * NPW * CHUNK;
-#pragma unroll 2
-            for (uint32_t j = 0; j < CHUNK / 2; j += 2) {
-                const uint4 w1 = lds_v4(sa + (j << 9));
-                const uint4 w2 = lds_v4(sa + ((j + 1) << 9));
-                const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
-                const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
-#pragma unroll
-                for (int nn = 0; nn < NPW; ++nn) {
-                    const uint32_t bw = lds_u32(sb0 + nn * CHUNK + (j << 1));  // pairs j and j + 1
-                    const uint32_t b1 = bw & 0xFFFFu, b2 = bw >> 16, b1h = bw << 16, b2h = bw & 0xFFFF0000u;
-#pragma unroll
-                    for (int q = 0; q < 4; ++q) {
-                        acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
-                        acc[nn][2 * q + 1] =
-                            sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
-                    }
-                }
+    // Work split over (tile, chunk) units in tile-major order, CTA b taking units
+    // [b * per, (b + 1) * per): whole tiles per CTA, or stream-K (per = total / CTAs: a CTA's
+    // run may end one tile and start the next, each segment closing with its own TMA reduce-add,
+    // and every SM stays busy whatever the tile count — whole tiles leave 20 of 148 SMs idle at
+    // 2048^3).  The choice weighs the per-chunk work, which grows with the share of listed pairs
+    // (read on the device from the prep kernel's count: no host round trip), against the
+    // per-segment epilogue: measured ~1 us + 55 us x density per chunk, ~3 us per epilogue
+    // (profiles/r2/satfix_streamk_r2.log).  `g` counts chunk stages across segments (parity).
+    const int64_t tiles = total_units / chunks;
+    const int64_t per_tiles = (tiles + gridDim.x - 1) / gridDim.x * chunks;
+    const int64_t per_stream = (total_units + gridDim.x - 1) / gridDim.x;
+    const float w = 1.0f + 55.0f * static_cast<float>(listed) / static_cast<float>(total_pairs), e = 3.0f;
+    const float cost_tiles = static_cast<float>(per_tiles) * w + static_cast<float>(per_tiles / chunks) * e;
+    const float cost_stream =
+        static_cast<float>(per_stream) * w + static_cast<float>((per_stream + chunks - 1) / chunks + 1) * e;
+    const int64_t units_per_cta = cost_stream < cost_tiles ? per_stream : per_tiles;
+    const int64_t u_begin = static_cast<int64_t>(blockIdx.x) * units_per_cta;
+    const int64_t u_end = min(total_units, u_begin + units_per_cta);
+    uint32_t g = 0;
+    for (int64_t pos = u_begin; pos < u_end;) {
+        const int64_t tile = pos / chunks;
+        const int64_t c_begin = pos - tile * chunks;
+        const int64_t c_end = min(min(chunks, c_begin + (u_end - pos)), c_begin + static_cast<int64_t>(MAX_LIST));
+        pos += c_end - c_begin;
+        const int64_t t = tile % tiles_n, u = tile / tiles_n;
+        __syncthreads();  // the previous segment's list and staging smem are done with
+        if (warp == 0) {  // the chunks with dangerous pairs, compacted by ballots
+            int cnt = 0;
+            for (int64_t cb = c_begin; cb < c_end; cb += 32) {
+                const int64_t c = cb + lane;
+                const bool hit = c < c_end && flags[t * chunks + c] != 0u;
+                const uint32_t bal = __ballot_sync(0xffffffffu, hit);
+                if (hit) list[cnt + __popc(bal & ((1u << lane) - 1u))] = static_cast<int>(c);
+                cnt += __popc(bal);
             }
-            __syncthreads();
-            continue;
+            if (lane == 0) *nlist_p = cnt;
         }
+        __syncthreads();
+        const int nl_count = *nlist_p;
+        if (nl_count == 0) continue;  // block-uniform: no dangerous pair in this segment
+
+        auto issue = [&](int i) {
+            const int s = (g + i) & 1;
+            const int64_t c = list[i];
+            uint8_t* st = smem + s * STAGE;
+            mbar_arrive_expect_tx(&full[s], STAGE);
+            bulk_load_1d(st, apm + (u * chunks + c) * (A_TILE / 4), A_TILE, &full[s]);
+            bulk_load_1d(st + A_TILE, bt + (t * chunks + c) * B_TILE, B_TILE, &full[s]);
+            bulk_load_1d(st + A_TILE + B_TILE, lt + (t * chunks + c) * L_TILE, L_TILE, &full[s]);
+        };
+        if (tid == 0) issue(0);
+
+        int32_t acc[NPW][8];  // [row of B][t]: A row l + 32 t
 #pragma unroll
-        for (int nn = 0; nn < NPW; ++nn) {
-            const int nl = warp * NPW + nn;
-            const uint32_t sb = st + A_TILE + nl * CHUNK;  // + j * 2: the row's pair j of B
-            const uint32_t sl = sc + TN + nl * (CHUNK / 2);
-            const int cnt = static_cast<int>(lds_u8(sc + nl));
-            // o1, o2: list entries = B byte offsets 2j; pair j of the lane's A rows sits at j * 512
-            auto process = [&](uint32_t o1, uint32_t o2, bool two) {
-                const uint4 w1 = lds_v4(sa + (o1 << 8));
-                const uint4 w2 = lds_v4(sa + (o2 << 8));
-                const uint32_t b1 = lds_u16(sb + o1);
-                const uint32_t b2 = two ? lds_u16(sb + o2) : 0u;
-                const uint32_t b1h = b1 << 16, b2h = b2 << 16;
-                const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
-                const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
+        for (int i = 0; i < NPW; ++i)
 #pragma unroll
-                for (int q = 0; q < 4; ++q) {
-                    acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
-                    acc[nn][2 * q + 1] = sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
-                }
-            };
-            if (cnt == CHUNK / 2) {  // every pair of the row listed (extreme inputs): no list walk
-#pragma unroll 4
+            for (int e = 0; e < 8; ++e) acc[i][e] = 0;
+
+        for (int i = 0; i < nl_count; ++i) {
+            // the other stage was released by the __syncthreads that ended iteration i - 1
+            if (tid == 0 && i + 1 < nl_count) issue(i + 1);
+            mbar_wait(&full[(g + i) & 1], ((g + i) >> 1) & 1);
+            // shared-window addresses: the loads below are plain LDS
+            const uint32_t st = smem_u32(smem) + ((g + i) & 1) * STAGE;
+            const uint32_t sa = st + lane * 16;             // + j * 512: pair j of this lane's 8 rows
+            const uint32_t sc = st + A_TILE + B_TILE;       // counts, then the index lists
+            // all 8 of this warp's rows fully listed (extreme inputs): pair-major loop, each pair of A
+            // words loaded once for the 8 rows instead of once per row
+            const uint32_t c_lo = lds_u32(sc + warp * NPW), c_hi = lds_u32(sc + warp * NPW + 4);
+            if (c_lo == 0x80808080u && c_hi == 0x80808080u) {
+                const uint32_t sb0 = st + A_TILE + warp * NPW * CHUNK;
+#pragma unroll 2
                 for (uint32_t j = 0; j < CHUNK / 2; j += 2) {
                     const uint4 w1 = lds_v4(sa + (j << 9));
                     const uint4 w2 = lds_v4(sa + ((j + 1) << 9));
-                    const uint32_t bw = lds_u32(sb + (j << 1));  // pairs j and j + 1 of B
-                    const uint32_t b1 = bw & 0xFFFFu, b2 = bw >> 16, b1h = bw << 16, b2h = bw & 0xFFFF0000u;
+                    const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+                    const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+                    for (int nn = 0; nn < NPW; ++nn) {
+                        const uint32_t bw = lds_u32(sb0 + nn * CHUNK + (j << 1));  // pairs j and j + 1
+                        const uint32_t b1 = bw & 0xFFFFu, b2 = bw >> 16, b1h = bw << 16, b2h = bw & 0xFFFF0000u;
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
+                            acc[nn][2 * q + 1] =
+                                sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
+                        }
+                    }
+                }
+                __syncthreads();
+                continue;
+            }
+#pragma unroll
+            for (int nn = 0; nn < NPW; ++nn) {
+                const int nl = warp * NPW + nn;
+                const uint32_t sb = st + A_TILE + nl * CHUNK;  // + j * 2: the row's pair j of B
+                const uint32_t sl = sc + TN + nl * (CHUNK / 2);
+                const int cnt = static_cast<int>(lds_u8(sc + nl));
+                // o1, o2: list entries = B byte offsets 2j; pair j of the lane's A rows sits at j * 512
+                auto process = [&](uint32_t o1, uint32_t o2, bool two) {
+                    const uint4 w1 = lds_v4(sa + (o1 << 8));
+                    const uint4 w2 = lds_v4(sa + (o2 << 8));
+                    const uint32_t b1 = lds_u16(sb + o1);
+                    const uint32_t b2 = two ? lds_u16(sb + o2) : 0u;
+                    const uint32_t b1h = b1 << 16, b2h = b2 << 16;
                     const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
                     const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
 #pragma unroll
                     for (int q = 0; q < 4; ++q) {
                         acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
-                        acc[nn][2 * q + 1] =
-                            sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
+                        acc[nn][2 * q + 1] = sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
+                    }
+                };
+                if (cnt == CHUNK / 2) {  // every pair of the row listed (extreme inputs): no list walk
+#pragma unroll 4
+                    for (uint32_t j = 0; j < CHUNK / 2; j += 2) {
+                        const uint4 w1 = lds_v4(sa + (j << 9));
+                        const uint4 w2 = lds_v4(sa + ((j + 1) << 9));
+                        const uint32_t bw = lds_u32(sb + (j << 1));  // pairs j and j + 1 of B
+                        const uint32_t b1 = bw & 0xFFFFu, b2 = bw >> 16, b1h = bw << 16, b2h = bw & 0xFFFF0000u;
+                        const uint32_t x1[4] = {w1.x, w1.y, w1.z, w1.w};
+                        const uint32_t x2[4] = {w2.x, w2.y, w2.z, w2.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            acc[nn][2 * q] = sat2_add(dp4a_us(x1[q], b1, 0), dp4a_us(x2[q], b2, 0), acc[nn][2 * q]);
+                            acc[nn][2 * q + 1] =
+                                sat2_add(dp4a_us(x1[q], b1h, 0), dp4a_us(x2[q], b2h, 0), acc[nn][2 * q + 1]);
+                        }
+                    }
+                } else {
+                    // whole groups of four entries, then a tail of up to three (no per-pair guards)
+                    const int full = cnt & ~3;
+                    for (int e = 0; e < full; e += 4) {
+                        const uint32_t idx = lds_u32(sl + e);
+                        process(__byte_perm(idx, 0, 0x4440), __byte_perm(idx, 0, 0x4441), true);
+                        process(__byte_perm(idx, 0, 0x4442), __byte_perm(idx, 0, 0x4443), true);
+                    }
+                    const int tail = cnt - full;
+                    if (tail != 0) {
+                        const uint32_t idx = lds_u32(sl + full);
+                        process(__byte_perm(idx, 0, 0x4440), __byte_perm(idx, 0, 0x4441), tail >= 2);
+                        if (tail == 3) process(__byte_perm(idx, 0, 0x4442), __byte_perm(idx, 0, 0x4442), false);
                     }
                 }
-            } else {
-                // whole groups of four entries, then a tail of up to three (no per-pair guards)
-                const int full = cnt & ~3;
-                for (int e = 0; e < full; e += 4) {
-                    const uint32_t idx = lds_u32(sl + e);
-                    process(__byte_perm(idx, 0, 0x4440), __byte_perm(idx, 0, 0x4441), true);
-                    process(__byte_perm(idx, 0, 0x4442), __byte_perm(idx, 0, 0x4443), true);
-                }
-                const int tail = cnt - full;
-                if (tail != 0) {
-                    const uint32_t idx = lds_u32(sl + full);
-                    process(__byte_perm(idx, 0, 0x4440), __byte_perm(idx, 0, 0x4441), tail >= 2);
-                    if (tail == 3) process(__byte_perm(idx, 0, 0x4442), __byte_perm(idx, 0, 0x4442), false);
-                }
+            }
+            __syncthreads();
+        }
+        g += static_cast<uint32_t>(nl_count);
+
+        // Epilogue: box (row block t, column block w / 4) of 32 x 32 int32, SWIZZLE_128B: row r's
+        // 16-byte chunk c sits at chunk c ^ (r & 7).  Lane l writes row l of 8 boxes (t = 0..7).
+        uint8_t* cs = smem;
+#pragma unroll
+        for (int tt = 0; tt < 8; ++tt) {
+            uint8_t* box = cs + (tt * (TN / 32) + (warp >> 2)) * 4096 + lane * 128;
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int chunk = ((warp & 3) * 2 + h) ^ (lane & 7);
+                *reinterpret_cast<int4*>(box + chunk * 16) =
+                    make_int4(acc[4 * h + 0][tt], acc[4 * h + 1][tt], acc[4 * h + 2][tt], acc[4 * h + 3][tt]);
             }
         }
+        fence_proxy_async_smem();
         __syncthreads();
-    }
-
-    // Epilogue: box (row block t, column block w / 4) of 32 x 32 int32, SWIZZLE_128B: row r's
-    // 16-byte chunk c sits at chunk c ^ (r & 7).  Lane l writes row l of 8 boxes (t = 0..7).
-    uint8_t* cs = smem;
-#pragma unroll
-    for (int tt = 0; tt < 8; ++tt) {
-        uint8_t* box = cs + (tt * (TN / 32) + (warp >> 2)) * 4096 + lane * 128;
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-            const int chunk = ((warp & 3) * 2 + h) ^ (lane & 7);
-            *reinterpret_cast<int4*>(box + chunk * 16) =
-                make_int4(acc[4 * h + 0][tt], acc[4 * h + 1][tt], acc[4 * h + 2][tt], acc[4 * h + 3][tt]);
+        if (tid == 0) {
+            for (int bx = 0; bx < (TM / 32) * (TN / 32); ++bx) {
+                const int rb = bx / (TN / 32), cb = bx % (TN / 32);
+                tma_reduce_add_2d(&tma_c, cs + bx * 4096, static_cast<int32_t>(t * TN + cb * 32),
+                                  static_cast<int32_t>(u * TM + rb * 32));
+            }
+            tma_store_commit();
+            tma_store_wait_read<0>();  // smem must outlive the reads; the adds complete with the grid
         }
-    }
-    fence_proxy_async_smem();
-    __syncthreads();
-    if (tid == 0) {
-        for (int bx = 0; bx < (TM / 32) * (TN / 32); ++bx) {
-            const int rb = bx / (TN / 32), cb = bx % (TN / 32);
-            tma_reduce_add_2d(&tma_c, cs + bx * 4096, static_cast<int32_t>(t * TN + cb * 32),
-                              static_cast<int32_t>(u * TM + rb * 32));
-        }
-        tma_store_commit();
-        tma_store_wait_read<0>();  // smem must outlive the reads; the adds complete with the grid
     }
 }
 

@@ -1043,25 +1043,14 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
         std::call_once(once[dev & 63], [&] { s = set_smem(sat_fix_kernel, SMEM); });
     }
     if (s == NGEMM_OK && !(skip & 16)) {
-        // One CTA per SM, so a launch runs in ceil(CTAs / SMs) waves; each CTA pays a fixed cost
-        // (chunk-list build, first load, epilogue reduce: ~one chunk's time) on top of its
-        // chunks.  Pick the K split minimising waves x (chunks per CTA + 1).
-        const int64_t tiles = tn * tm;
-        int64_t splits = 1;
-        double best = 1e30;
-        for (int64_t sp = 1; sp <= std::min<int64_t>(chunks, 16); ++sp) {
-            const int64_t per_sp = (chunks + sp - 1) / sp;
-            const double t = static_cast<double>((tiles * sp + di.sms - 1) / di.sms) * static_cast<double>(per_sp + 1);
-            if (t < best - 1e-9) best = t, splits = sp;
-        }
-        splits = std::max<int64_t>(splits, (chunks + MAX_LIST - 1) / MAX_LIST);  // the CTA's chunk list fits
-        const int64_t per = (chunks + splits - 1) / splits;
-        splits = (chunks + per - 1) / per;
-        dim3 grid(static_cast<unsigned>(tn), static_cast<unsigned>(tm), static_cast<unsigned>(splits));
-        if (tm > 65535 || splits > 65535) s = fail(NGEMM_ERR_SHAPE, "sat fix: M or K too large");
-        else
-            s = launched(launch_k(sat_fix_kernel, grid, dim3(THREADS), SMEM, st, 1, 1, tcm, apm, bt, lt, flags, chunks,
-                                  per, guard));
+        // Stream-K over (tile, chunk) units, one CTA per SM (kernel_satfix.cuh): every SM gets
+        // the same number of chunk units whatever the tile count; a CTA's run may end one tile
+        // and start the next, each segment closing with its own TMA reduce-add into C.
+        const int64_t total = tn * tm * chunks;
+        const int64_t grid = std::max<int64_t>(1, std::min<int64_t>(total, di.sms));
+        const int64_t total_pairs = tn * TN * chunks * (CHUNK / 2);  // listable (B row, pair) slots
+        s = launched(launch_k(sat_fix_kernel, dim3(static_cast<unsigned>(grid)), dim3(THREADS), SMEM, st, 1, 1, tcm,
+                              apm, bt, lt, flags, chunks, tn, total, total_pairs, guard));
     }
     cudaFreeAsync(buf, st);
     return s;
