@@ -320,8 +320,11 @@ ngemm_status host_pipeline(const HostGemm& g) {
     std::atomic<bool> out_failed{false};
     std::string out_msg;
     std::thread out_thread;
+    int dev_main = 0;
+    cudaGetDevice(&dev_main);
     if (stage_out && s == NGEMM_OK) {
         out_thread = std::thread([&] {
+            cudaSetDevice(dev_main);  // a new thread starts on device 0; the streams and events are dev_main's
             auto ck = [&](cudaError_t e, const char* what) {
                 if (e != cudaSuccess && !out_failed.exchange(true)) out_msg = std::string(what) + ": " + cudaGetErrorString(e);
                 return e == cudaSuccess;
