@@ -56,3 +56,22 @@ def test_our_arm_json_line():
     assert d["e2e"]["h2d_bytes_per_step"] == 2 * 1024 * 1024 and d["e2e"]["d2h_bytes_per_step"] == 4 * 1024 * 1024
     assert d["cpu_baseline"]["cores"] >= 1 and d["cpu_baseline"]["kind"] in ("reference", "port")
     assert "sm_mhz" in d["clocks"] and "reasons" in d["clocks"]
+
+
+def test_reference_arm_config_and_data_match_ours():
+    """The driver compares the two arms' `config` (same_config) and `data`: both come from the
+    same functions (bench.config_dict / bench.data_desc), the reference arm's line must equal what
+    our arm prints for the same arguments, and both arms draw the same seeded inputs."""
+    import argparse
+    import numpy as np
+    sys.path.insert(0, ROOT)
+    import bench
+    lines = run_bench("--impl", "reference", "--config", "c1", "--steps", "1", "--warmup", "1")
+    d = lines[0]
+    args = argparse.Namespace(shape=None, config="c1", mode="exact", adist="uniform", bdist="auto")
+    assert d["config"] == bench.config_dict(args, 1)
+    assert d["data"] == bench.data_desc(args, 1024)
+    a1, a2 = bench.gen_a(64, 100, "uniform"), bench.gen_a(64, 100, "uniform")
+    assert np.array_equal(a1, a2) and a1.dtype == np.uint8
+    b = bench.gen_b(50, 100, "normal")
+    assert b.dtype == np.int8 and abs(float(b.astype(np.float64).std()) - 32.0) < 3.0
