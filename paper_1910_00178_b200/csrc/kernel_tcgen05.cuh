@@ -47,8 +47,14 @@ struct Smem {
     static constexpr int A_BYTES = BM * BK;
     static constexpr int B_BYTES = (BN / CG) * BK;
     static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-    static constexpr int TMEM_COLS = (2 * BN <= 32) ? 32 : (2 * BN <= 64) ? 64 : (2 * BN <= 128) ? 128
-                                   : (2 * BN <= 256) ? 256 : 512;
+    // BN <= 256: two accumulators (the epilogue of one tile overlaps the next tile's MMAs);
+    // BN = 512: one accumulator over all 512 TMEM columns (25 % less L2->SM operand traffic per
+    // MAC than 256 x 256; the epilogue overlaps only the next tile's first loads)
+    static constexpr int NACC = BN > 256 ? 1 : 2;
+    static constexpr int MMA_N = BN > 256 ? 256 : BN;  // UMMA N <= 256: BN = 512 issues two per K step
+    static constexpr int TMEM_COLS = (NACC * BN <= 32) ? 32 : (NACC * BN <= 64) ? 64 : (NACC * BN <= 128) ? 128
+                                   : (NACC * BN <= 256) ? 256 : 512;
+    static_assert(NACC * BN <= 512, "the accumulators must fit the 512 TMEM columns");
     // epilogue staging: 4 warps x 2 buffers x (32 rows x 32 int32) in SWIZZLE_128B order
     static constexpr int STAGE_C_BYTES = 32 * 32 * 4;
     static constexpr int C_OFFSET = STAGES * STAGE_BYTES;
@@ -261,8 +267,8 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
     } else if (warp == 1) {
         if (lane == 0 && rank == 0) {
             // ---------------- MMA issuer (single thread of the leader CTA)
-            const uint32_t idesc_full = idesc_i8(UMMA_M, BN, map.a_signed != 0, map.b_signed != 0);
-            const uint32_t idesc_half = idesc_i8(UMMA_M, BN / 2, map.a_signed != 0, map.b_signed != 0);
+            const uint32_t idesc_full = idesc_i8(UMMA_M, S::MMA_N, map.a_signed != 0, map.b_signed != 0);
+            const uint32_t idesc_half = idesc_i8(UMMA_M, S::MMA_N / 2, map.a_signed != 0, map.b_signed != 0);
             int s = 0;
             uint32_t ph = 0;
             int acc = 0;
@@ -283,10 +289,16 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                     const uint32_t sa = smem_u32(smem + s * S::A_BYTES);
                     const uint32_t sb = smem_u32(smem + STAGES * S::A_BYTES + s * S::B_BYTES);
 #pragma unroll
-                    for (int k = 0; k < tc::BK / tc::UMMA_K; ++k) {
-                        if (map.dbg & 2) break;
-                        mma_i8<CG>(d_tmem, sdesc_k_sw128(sa + k * tc::UMMA_K), sdesc_k_sw128(sb + k * tc::UMMA_K),
-                                   idesc, (kb > kb0 || k > 0) ? 1u : 0u);
+                    for (int h = 0; h < BN / S::MMA_N; ++h) {
+                        // BN = 512: MMA h reads rows [128h, 128h + 128) of each CTA's B slab (this
+                        // CTA's 256 rows of B) and accumulates into TMEM columns [256h, 256h + 256)
+#pragma unroll
+                        for (int k = 0; k < tc::BK / tc::UMMA_K; ++k) {
+                            if (map.dbg & 2) break;
+                            mma_i8<CG>(d_tmem + h * S::MMA_N, sdesc_k_sw128(sa + k * tc::UMMA_K),
+                                       sdesc_k_sw128(sb + h * (S::MMA_N / CG) * tc::BK + k * tc::UMMA_K), idesc,
+                                       (kb > kb0 || k > 0) ? 1u : 0u);
+                        }
                     }
                     if constexpr (CG == 1 && MC == 1) mma_commit(&empty[s]);
                     else if constexpr (CG == 1) mma_commit_mc(&empty[s], static_cast<uint16_t>(0x3));  // both read A
@@ -295,8 +307,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 }
                 if constexpr (CG == 1) mma_commit(&tfull[acc]);
                 else mma_commit_cg2_mc(&tfull[acc], pair_mask);
-                acc ^= 1;
-                if (acc == 0) acc_ph ^= 1;
+                if (++acc == S::NACC) { acc = 0; acc_ph ^= 1; }
             }
             TC_TRACE_NOW(6);
         }
@@ -322,18 +333,17 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
             if (t == unit && warp == 4 && lane == 0) TC_TRACE_NOW(7);
             const int row0 = tm * UMMA_M + static_cast<int>(rank) * tc::BM + ew * 32;
             const uint32_t taddr = tmem_base + acc * BN + (static_cast<uint32_t>(ew * 32) << 16);
-#pragma unroll 1
-            for (int c = 0; c < ncols; c += 32) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(taddr + c, v);
-                tmem_wait_ld();
+            // one 32-column chunk of this warp's 32 accumulator rows: registers -> C
+            auto emit = [&](uint32_t (&v)[32], const int c) {
                 if (t == unit && c == 0 && warp == 4 && lane == 0) TC_TRACE_NOW(10);
-                if (!has_k || row0 >= M) continue;
+                if (!has_k || row0 >= M) return;
                 if (map.shift) {
 #pragma unroll
                     for (int j = 0; j < 32; ++j) v[j] <<= map.shift;  // mod 2^32, like the accumulator
                 }
-                const int col0 = col_base + c;
+                // BN = 512 (pairs): TMEM columns [256h + 128r, 256h + 128r + 128) hold tile columns
+                // [256r + 128h, +128) — CTA r's B slab is tile columns [256r, 256r + 256)
+                const int col0 = col_base + (BN > 256 ? ((c >> 7) & 1) * 256 + (c >> 8) * 128 + (c & 127) : c);
                 if (c_mode == 4) {
                     // fused requantisation to int8: each lane loads one column's scale / bias and
                     // the warp broadcasts them; lane = row, 32 int8 per row, two 16-byte stores
@@ -361,7 +371,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                                 if (col0 + j < N) orow[j] = static_cast<int8_t>((packed[j >> 2] >> (8 * (j & 3))) & 0xFFu);
                         }
                     }
-                    continue;
+                    return;
                 }
                 if (c_mode <= 1) {
                     uint8_t* buf = stage_c + cbuf * S::STAGE_C_BYTES;
@@ -402,6 +412,22 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                         }
                     }
                 }
+            };
+            // two register sets: the tcgen05.ld of the next chunk is in flight while this one is
+            // staged and stored (tcgen05.wait::ld waits for every outstanding load, so the next
+            // load is issued right after the wait)
+            uint32_t va[32], vb[32];
+            tmem_ld_32x32b_x32(taddr, va);
+#pragma unroll 1
+            for (int c = 0; c < ncols; c += 64) {
+                tmem_wait_ld();
+                if (c + 32 < ncols) tmem_ld_32x32b_x32(taddr + c + 32, vb);
+                emit(va, c);
+                if (c + 32 < ncols) {
+                    tmem_wait_ld();
+                    if (c + 64 < ncols) tmem_ld_32x32b_x32(taddr + c + 64, va);
+                    emit(vb, c + 32);
+                }
             }
             if (t == unit && warp == 4 && lane == 0) TC_TRACE_NOW(12);
             tc_fence_before();
@@ -410,8 +436,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
                 if constexpr (CG == 1) mbar_arrive(&tempty[acc]);
                 else mbar_arrive_cluster(&tempty[acc], leader);
             }
-            acc ^= 1;
-            if (acc == 0) acc_ph ^= 1;
+            if (++acc == S::NACC) { acc = 0; acc_ph ^= 1; }
         }
         // the staging smem must be read out before the CTA exits; the global writes themselves
         // complete before the grid does (and before a dependent grid's griddepcontrol.wait)

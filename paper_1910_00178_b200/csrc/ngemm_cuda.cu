@@ -733,7 +733,8 @@ ngemm_status make_tmap_c(CUtensorMap* map, const int32_t* c, int64_t rows, int64
 enum TcCfg {
     TC_PAIR256 = 0, TC_1CTA256 = 1, TC_1CTA128 = 2, TC_1CTA64 = 3, TC_QUAD256 = 4, TC_LEAN128 = 5, TC_LEAN64 = 6,
     TC_MC128 = 7, TC_MC64 = 8,  // 1-CTA tiles in 2-CTA clusters sharing A by TMA multicast
-    TC_NUM_CFG = 9
+    TC_PAIR512 = 9,             // 256x512 per pair, one accumulator over all 512 TMEM columns
+    TC_NUM_CFG = 10
 };
 struct TcCfgInfo {
     int cg, bn, mc;
@@ -750,6 +751,7 @@ constexpr TcCfgInfo kTcCfg[TC_NUM_CFG] = {
     {1, 64, 1, 330.0, 1},   // 128x64, 3 stages
     {1, 128, 2, 300.0, 0},  // 128x128 x 2 CTAs sharing A: half the A traffic into each SM
     {1, 64, 2, 192.0, 0},   // 128x64 x 2 CTAs sharing A
+    {2, 512, 1, 1024.0, 0}, // 256x512x128 per pair: 96 KB of operands per 16.8 M MACs (pairs of 256x256: 128 KB)
 };
 // Lean configurations fit two CTAs per SM, so under PDL the next grid's CTAs finish their setup
 // while the previous grid runs — but their 2-3 stage pipelines lose more in the K loop than the
@@ -777,6 +779,7 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
         const int64_t tiles_n = (n + ci.bn - 1) / ci.bn;
         if (ci.mc > 1 && (tiles_n % ci.mc != 0 || quad_disabled())) continue;
         if (ci.lean) continue;
+        if (cfg == TC_PAIR512) continue;  // chosen by the rule below the loop
         const int64_t tiles = ((m + 128 * ci.cg - 1) / (128 * ci.cg)) * tiles_n / ci.mc;
         const int64_t units = sms / (ci.cg * ci.mc);
         for (int splits = 1; splits <= 16; splits *= 2) {
@@ -795,6 +798,17 @@ TcPlan plan_tcgen05(int64_t m, int64_t n, int64_t k, int sms, int c_mode_ok) {
                 best = {cfg, splits};
             }
         }
+    }
+    // 256x512 pair tiles (one accumulator over all 512 TMEM columns): 25 % less L2->SM operand
+    // traffic per MAC, but the epilogue no longer overlaps the next tile's MMAs (~7 us per tile) —
+    // ahead for deep K and many waves (profiles/r2/pair512_ab_r2.log, pair512_ksweep_r2.log:
+    // 16384^3 +5.5 %, 8192^3 +3 %, K = 4096 equal, K <= 2048 behind)
+    if (best.cfg == TC_PAIR256 && best.splits == 1 && k >= 8192) {
+        const int64_t units = sms / 2;
+        const int64_t tm = (m + 255) / 256;
+        const int64_t w256 = (tm * ((n + 255) / 256) + units - 1) / units;
+        const int64_t w512 = (tm * ((n + 511) / 512) + units - 1) / units;
+        if (w512 >= 4 && 2.0 * 0.95 * static_cast<double>(w512) < static_cast<double>(w256)) best.cfg = TC_PAIR512;
     }
     if (opt(O_TC_CFG) >= 0) best.cfg = opt(O_TC_CFG) % TC_NUM_CFG;  // experiments / tests
 
@@ -918,7 +932,7 @@ ngemm_status launch_tc_t(const CUtensorMap& ta, const CUtensorMap& tb, const CUt
     // by per-SM MMA time, so the idle SMs of a short last wave cost little.  Off by default.
     map.full_tiles = tiles * map.splits;
     const int rem = tiles % units;
-    if (MC == 1 && map.splits == 1 && rem > 0 && 2 * rem <= units && opt(O_TC_SCHED) == 1) map.full_tiles = tiles - rem;
+    if (MC == 1 && BN <= 256 && map.splits == 1 && rem > 0 && 2 * rem <= units && opt(O_TC_SCHED) == 1) map.full_tiles = tiles - rem;
     const int work = map.full_tiles + 2 * (tiles * map.splits - map.full_tiles);
     const int grid = std::min(work, units) * CG * MC;
     NG_LAUNCH(kern, dim3(grid), dim3(tc::THREADS), S::TOTAL, st, CG * MC, 1, ta, tb, tbh, tcmap, c, ldc,
@@ -963,6 +977,7 @@ ngemm_status launch_tcgen05(const uint8_t* a, int64_t lda, const int8_t* b, int6
         case TC_LEAN64: s = launch_tc_t<64, 3, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         case TC_MC128: s = launch_tc_t<128, 6, 1, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         case TC_MC64: s = launch_tc_t<64, 8, 1, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
+        case TC_PAIR512: s = launch_tc_t<512, 4, 2>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         default: s = launch_tc_t<64, 8, 1>(ta, tb, tbh, tcm, c, ldc, m, n, k, plan.splits, c_mode, di, st, ops); break;
         }
     }

@@ -358,7 +358,7 @@ def test_config5_full_size(cuda, oracle, golden, mode):
         assert torch.equal(lhs, rhs)
 
 
-@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6, 7, 8])
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, knobs):
     """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64, the 4-CTA and 2-CTA
     A-multicast clusters, the lean 2-3 stage variants), with and without
