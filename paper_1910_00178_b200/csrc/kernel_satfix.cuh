@@ -98,12 +98,19 @@ __global__ void sat_prep_a_kernel(const uint8_t* __restrict__ a, int64_t lda, in
 }
 
 // B -> B_safe (row-major, pitch lds, dangerous pairs zeroed: the tensor-core operand), B_t,
-// L_t, flags and the dangerous-pair count (guard[4..5]).  Thread = (tile t, chunk c, row r, 64-byte quarter q) with q fastest, so a
-// warp covers 8 rows of one tile chunk and reduces its count into one atomic per flag.
-__global__ void sat_prep_b_kernel(const int8_t* __restrict__ b, int64_t ldb, int64_t n, int64_t k, int vec_ok,
-                                  int64_t chunks, uint8_t* __restrict__ bsafe, int64_t lds, uint8_t* __restrict__ bt,
-                                  uint8_t* __restrict__ lt, uint32_t* __restrict__ flags, int32_t* __restrict__ guard) {
+// L_t, flags and the dangerous-pair count (guard[4..5]).  Thread = (tile t, chunk c, row r,
+// 16-byte piece q) with q fastest: the 16 lanes of a half warp cover one row's 256-byte chunk
+// (coalesced 256-byte loads and stores), a segmented scan over them places each lane's entries
+// in the row's index list, and a block (16 rows of ONE tile chunk: 128 rows = 8 blocks) adds
+// its count to the tile chunk's flag with one atomic.  One short item per thread (N K / 16
+// threads), so the kernel is bandwidth- rather than latency-bound (the 64-byte-per-thread
+// version took 21.7 us for a 4 MiB B: profiles/r2/launches_c4_satfix_ext_r2_final.csv).
+__global__ void __launch_bounds__(256)
+    sat_prep_b_kernel(const int8_t* __restrict__ b, int64_t ldb, int64_t n, int64_t k, int vec_ok, int64_t chunks,
+                      uint8_t* __restrict__ bsafe, int64_t lds, uint8_t* __restrict__ bt, uint8_t* __restrict__ lt,
+                      uint32_t* __restrict__ flags, int32_t* __restrict__ guard) {
     using namespace satfix;
+    __shared__ uint32_t blk_cnt;
     pdl_launch_dependents();
     pdl_wait();
     const int64_t amax = guard[0];
@@ -112,61 +119,59 @@ __global__ void sat_prep_b_kernel(const int8_t* __restrict__ b, int64_t ldb, int
     const uint32_t neg_lim = amax ? static_cast<uint32_t>(32768 / amax) : 0xFFFFu;
     const uint8_t* bu = reinterpret_cast<const uint8_t*>(b);
     const int64_t tiles = (n + TN - 1) / TN;
-    const int64_t total = tiles * chunks * TN * 4;  // a multiple of 512: whole warps per item range
-    unsigned long long cnt_all = 0;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const int q = static_cast<int>(i & 3);
-        const int r = static_cast<int>((i >> 2) & (TN - 1));
-        const int64_t tc = i >> 9;  // t * chunks + c
+    const int64_t total = tiles * chunks * TN * 16;  // a multiple of 2048: whole blocks per tile chunk
+    unsigned long long cnt_all = 0;  // thread 0 of the block only
+    for (int64_t base = blockIdx.x * static_cast<int64_t>(blockDim.x); base < total;
+         base += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+        const int64_t i = base + threadIdx.x;
+        const int q = static_cast<int>(i & 15);
+        const int r = static_cast<int>((i >> 4) & (TN - 1));
+        const int64_t tc = i >> 11;  // t * chunks + c  (block-uniform: 256 threads = 16 rows of it)
         const int64_t t = tc / chunks, c = tc - t * chunks;
-        const int64_t row = t * TN + r, c0 = c * CHUNK + q * 64;
+        const int64_t row = t * TN + r, c0 = c * CHUNK + q * 16;
+        if (threadIdx.x == 0) blk_cnt = 0;
+        __syncthreads();
+        const uint4 orig = simt_load16<true>(bu, ldb, row, n, c0, k, vec_ok);
+        uint32_t w[4] = {orig.x, orig.y, orig.z, orig.w};
         uint32_t mask = 0;
-        uint4 orig[4], safe[4];
 #pragma unroll
-        for (int h = 0; h < 4; ++h) {
-            orig[h] = simt_load16<true>(bu, ldb, row, n, c0 + 16 * h, k, vec_ok);
-            uint32_t w[4] = {orig[h].x, orig[h].y, orig[h].z, orig[h].w};
-#pragma unroll
-            for (int e = 0; e < 4; ++e) {
-                uint32_t pos, neg;
-                pair_pos_neg(w[e], pos, neg);
-                const bool d0 = (pos & 0xFFFFu) > pos_lim || (neg & 0xFFFFu) > neg_lim;
-                const bool d1 = (pos >> 16) > pos_lim || (neg >> 16) > neg_lim;
-                mask |= (d0 ? 1u : 0u) << (h * 8 + e * 2);
-                mask |= (d1 ? 1u : 0u) << (h * 8 + e * 2 + 1);
-                w[e] &= (d0 ? 0u : 0x0000FFFFu) | (d1 ? 0u : 0xFFFF0000u);
-            }
-            safe[h] = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int e = 0; e < 4; ++e) {
+            uint32_t pos, neg;
+            pair_pos_neg(w[e], pos, neg);
+            const bool d0 = (pos & 0xFFFFu) > pos_lim || (neg & 0xFFFFu) > neg_lim;
+            const bool d1 = (pos >> 16) > pos_lim || (neg >> 16) > neg_lim;
+            mask |= (d0 ? 1u : 0u) << (e * 2);
+            mask |= (d1 ? 1u : 0u) << (e * 2 + 1);
+            w[e] &= (d0 ? 0u : 0x0000FFFFu) | (d1 ? 0u : 0xFFFF0000u);
         }
-        uint4* dt = reinterpret_cast<uint4*>(bt + tc * B_TILE + r * CHUNK + q * 64);
-#pragma unroll
-        for (int h = 0; h < 4; ++h) dt[h] = orig[h];
-        if (row < n) {
-            uint4* ds = reinterpret_cast<uint4*>(bsafe + row * lds + c0);
-#pragma unroll
-            for (int h = 0; h < 4; ++h) ds[h] = safe[h];
-        }
-        // the row's index list: the 4 quarters of a row are 4 consecutive lanes
+        *reinterpret_cast<uint4*>(bt + tc * B_TILE + r * CHUNK + q * 16) = orig;
+        if (row < n) *reinterpret_cast<uint4*>(bsafe + row * lds + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+        // the row's index list: inclusive scan of the popcounts over the row's 16 lanes
         const uint32_t mine = __popc(mask);
-        uint32_t before = __shfl_up_sync(0xffffffffu, mine, 1, 4);
-        if (q < 1) before = 0;
-        uint32_t b2 = __shfl_up_sync(0xffffffffu, before + mine, 2, 4);
-        const uint32_t off = (q < 2 ? before : before + b2);
-        const uint32_t row_total = __shfl_sync(0xffffffffu, off + mine, 3, 4);
+        uint32_t incl = mine;
+#pragma unroll
+        for (int o = 1; o < 16; o <<= 1) {
+            const uint32_t up = __shfl_up_sync(0xffffffffu, incl, o, 16);
+            if (q >= o) incl += up;
+        }
+        const uint32_t row_total = __shfl_sync(0xffffffffu, incl, 15, 16);
         uint8_t* rec = lt + tc * L_TILE;
         if (q == 0) rec[r] = static_cast<uint8_t>(row_total);  // 0..128
-        uint8_t* lst = rec + TN + r * (CHUNK / 2) + off;
+        uint8_t* lst = rec + TN + r * (CHUNK / 2) + (incl - mine);
         // entries are B byte offsets 2j (<= 254): the fix kernel uses them unmasked — any byte,
         // even a stale one past the count, addresses inside the row and inside the A tile
-        for (uint32_t mb = mask, i = 0; mb; mb &= mb - 1, ++i)
-            lst[i] = static_cast<uint8_t>(2 * (q * 32 + __ffs(mb) - 1));
-        unsigned long long cnt = mine;
-        for (int o = 16; o > 0; o >>= 1) cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
-        if ((threadIdx.x & 31) == 0 && cnt) atomicAdd(&flags[tc], static_cast<uint32_t>(cnt));
-        cnt_all += cnt;
+        for (uint32_t mb = mask, e = 0; mb; mb &= mb - 1, ++e)
+            lst[e] = static_cast<uint8_t>(2 * (q * 8 + __ffs(mb) - 1));
+        // two rows per warp -> one shared-memory add per warp, one global atomic per block
+        const uint32_t other = __shfl_sync(0xffffffffu, row_total, 16);
+        if ((threadIdx.x & 31) == 0 && row_total + other) atomicAdd(&blk_cnt, row_total + other);
+        __syncthreads();
+        if (threadIdx.x == 0 && blk_cnt) {
+            atomicAdd(&flags[tc], blk_cnt);
+            cnt_all += blk_cnt;
+        }
     }
-    if ((threadIdx.x & 31) == 0 && cnt_all) atomicAdd(reinterpret_cast<unsigned long long*>(guard + 4), cnt_all);
+    if (threadIdx.x == 0 && cnt_all) atomicAdd(reinterpret_cast<unsigned long long*>(guard + 4), cnt_all);
 }
 
 // acc += sat16(p0) + sat16(p1) (cvt.pack.sat.s16.s32 clamps both, dp2a adds the halves).

@@ -1047,7 +1047,7 @@ ngemm_status launch_sat_hybrid(const uint8_t* a, int64_t lda, const int8_t* b, i
         s = launched(launch_k(sat_prep_a_kernel, grid_for(tm * chunks * 8 * (TM / 2)), dim3(256), 0, st, 1, 1, a, lda,
                               m, k, va, chunks, apm, guard));
     if (s == NGEMM_OK && !(skip & 2))
-        s = launched(launch_k(sat_prep_b_kernel, grid_for(tn * chunks * TN * 4), dim3(256), 0, st, 1, 1, b, ldb, n, k,
+        s = launched(launch_k(sat_prep_b_kernel, grid_for(tn * chunks * TN * 16), dim3(256), 0, st, 1, 1, b, ldb, n, k,
                               vb, chunks, bsafe, lds, bt, lt, flags, guard));
     if (s == NGEMM_OK && !(skip & 8))
         s = launch_tcgen05(a, lda, reinterpret_cast<const int8_t*>(bsafe), lds, c, ldc, m, n, k, di, st);
