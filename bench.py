@@ -262,7 +262,7 @@ def load_traffic(tag):
 NCU_TAGS = {"tcgen05:16384x16384x16384:exact": "r2/ncu_c5_tc512_r2.json", "tcgen05:1024x1024x1024:exact": "r2/ncu_c1_tc_r2.json",
             "tcgen05:2048x4096x1024:exact": "r2/ncu_c3_tc_r2.json", "tcgen05:2048x2048x2048:exact": "r2/ncu_c4_tc_r2.json",
             "skinny:16x4096x1024:exact": "r2/ncu_c2_mma_r2.json", "skinny:1x4096x1024:exact": "ncu_c2_mma_m1.json",
-            "skinny:16x4096x1024:sat": "r2/ncu_c2_sat_r2.json"}
+            "skinny:16x4096x1024:sat": "r2/ncu_c2_sathyb_r2.json"}
 
 
 def load_ncu(tag):

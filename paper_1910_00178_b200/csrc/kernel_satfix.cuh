@@ -174,15 +174,6 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0 && cnt_all) atomicAdd(reinterpret_cast<unsigned long long*>(guard + 4), cnt_all);
 }
 
-// acc += sat16(p0) + sat16(p1) (cvt.pack.sat.s16.s32 clamps both, dp2a adds the halves).
-__device__ __forceinline__ int32_t sat2_add(int32_t p0, int32_t p1, int32_t acc) {
-    uint32_t packed;
-    asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(packed) : "r"(p1), "r"(p0));
-    int32_t r;
-    asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(packed), "r"(0x0101), "r"(acc));
-    return r;
-}
-
 // The sparse fix: C[m][n] += sum over the dangerous pairs j of row n of
 // sat16(A[m][2j] B[n][2j] + A[m][2j+1] B[n][2j+1]), after the tensor-core kernel stored
 // C = A . B_safe.

@@ -670,3 +670,268 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? (BMASK ? 2 : (MT <= 4
 }
 
 }  // namespace ngemm_dev
+
+namespace ngemm_dev {
+
+// ---------------------------------------------------------------------------------------------
+// skinny_sathyb_kernel — HardwareSaturating skinny GEMM (4 < M <= 16) on the warp-level tensor
+// cores plus a sparse fix, the M <= 16 counterpart of kernel_satfix.cuh.
+//
+// A is unsigned (<= 255), so a pair (b0, b1) of B can only clamp when both bytes have the same
+// sign and |b0 + b1| >= 129: with opposite signs (or a zero) the pair sum stays inside
+// [255 * -128, 255 * 127]; with equal signs its extreme is 255 * (b0 + b1), and 255 * 128 = 32640
+// still fits int16.  Every other pair contributes its exact product, so
+//     C_sat = A . B (exact, mma.sync as in skinny_mma_kernel) + sum over listed pairs of (sat16(s) - s).
+// The load stream and fragment mapping are skinny_mma_kernel's.  Per 128-byte chunk each lane
+// tests its 16 B words (two dp4a against 0x0101 give b0 + b1 + 128 and b2 + b3 + 128; one unsigned
+// compare each), the warp counts the listed words (redux) and takes one of two warp-uniform paths:
+//   sparse (<= QCAP listed words; weight-like B, sigma = 32: ~4 of 512): the exact MMAs, then the
+//       listed words go to a per-warp queue in shared memory and (word, A row) units are spread
+//       over the lanes — each adds its correction to corr[row][m] (shared-memory atomic, only when
+//       a pair really clamps);
+//   dense (uniform int8 B: ~44 % of the words): no MMA; the chunk's saturating sums are computed
+//       with the dp4a / cvt.pack.sat / dp2a step of skinny_sat_kernel, one A row at a time (rolled
+//       loop), into this lane's private cells of part[warp][t][row][m].
+// At the end every lane adds its MMA fragment into its own part cells as well, and the CTA sums
+// part over warps and K phases plus corr.  All terms wrap mod 2^32, so the result is bit-exact.
+// ---------------------------------------------------------------------------------------------
+namespace skinny_sathyb {
+constexpr int QCAP = 128;  // queue entries per warp; more listed words than this -> dense path
+template <int MT, int WARPS>
+struct Smem {
+    static constexpr int PART = WARPS * 4 * 16 * MT * 4;  // [warp][t][row][m] int32
+    static constexpr int QUEUE = WARPS * QCAP * 8;        // [warp][entry]{word, meta}
+    static constexpr int CORR = 16 * MT * 4;              // [row][m]
+    static constexpr int TOTAL = PART + QUEUE + CORR + 16;  // + the "a warp took the dense path" flag
+};
+}  // namespace skinny_sathyb
+
+template <int MT, int WARPS>
+__global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
+    skinny_sathyb_kernel(const uint8_t* __restrict__ A, int64_t lda, const int8_t* __restrict__ B, int64_t ldb,
+                         int32_t* __restrict__ C, int64_t ldc, int M, int64_t N, int64_t K, int64_t k_range,
+                         int vec_ok, int accumulate, int64_t batch_sa, int64_t batch_sb, int64_t batch_sc) {
+    using S = skinny_sathyb::Smem<MT, WARPS>;
+    constexpr int NB = MT / 8;
+    constexpr int QCAP = skinny_sathyb::QCAP;
+    extern __shared__ __align__(16) uint8_t sathyb_smem[];
+    int32_t* part = reinterpret_cast<int32_t*>(sathyb_smem);
+    uint2* queue = reinterpret_cast<uint2*>(sathyb_smem + S::PART);
+    int32_t* corr = reinterpret_cast<int32_t*>(sathyb_smem + S::PART + S::QUEUE);
+    int* dense_used = reinterpret_cast<int*>(sathyb_smem + S::PART + S::QUEUE + S::CORR);
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int g = lane >> 2, t = lane & 3;
+    pdl_launch_dependents();
+    A += blockIdx.z * batch_sa;
+    B += blockIdx.z * batch_sb;
+    C += blockIdx.z * batch_sc;
+    const int64_t kbeg = static_cast<int64_t>(blockIdx.y) * k_range;
+    const int64_t kend = min(K, kbeg + k_range);
+    const int64_t n0 = static_cast<int64_t>(blockIdx.x) * 16;
+    if (vec_ok & 2) {  // warm L2 before the dependency wait, as in skinny_mma_kernel
+        const uint32_t span = static_cast<uint32_t>((kend - kbeg) & ~int64_t(15));
+        if (span != 0) {
+            if (tid < 16) {
+                if (n0 + tid < N) prefetch_l2_bulk(reinterpret_cast<const uint8_t*>(B) + (n0 + tid) * ldb + kbeg, span);
+            } else if (tid < 16 + M) {
+                prefetch_l2_bulk(A + (tid - 16) * lda + kbeg, span);
+            }
+        }
+    }
+    // this lane's private cells part[warp][t][g + 8r][m], and the shared corrections
+    int32_t* my_part = part + ((warp * 4 + t) * 16 + g) * MT;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) my_part[m] = my_part[8 * MT + m] = 0;
+    for (int i = tid; i < 16 * MT; i += WARPS * 32) corr[i] = 0;
+    if (tid == 0) *dense_used = 0;
+    __syncthreads();
+    pdl_wait();
+    const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
+    const bool vec = vec_ok != 0;
+    const int64_t kt = kbeg + t * 16;
+    const int64_t rem = kend - kt;
+    const uint8_t* pb = Bu + (n0 + g) * ldb + kt;
+    const bool ok_b0 = n0 + g < N, ok_b1 = n0 + g + 8 < N;
+    uint2* my_queue = queue + warp * QCAP;
+
+    int32_t d[NB][4];
+#pragma unroll
+    for (int j = 0; j < NB; ++j) d[j][0] = d[j][1] = d[j][2] = d[j][3] = 0;
+    int32_t dacc[2][MT];  // dense path: rows {g, g+8} x A rows, this lane's K phase
+#pragma unroll
+    for (int m = 0; m < MT; ++m) dacc[0][m] = dacc[1][m] = 0;
+    bool used_dense = false;
+
+    // 16 bytes of A row m at this lane's K phase of chunk offset o (zero past the K range)
+    auto load_a = [&](int m, int64_t o, bool fast) {
+        const uint8_t* p = A + static_cast<int64_t>(m) * lda + kt + o;
+        if (fast) return __ldg(reinterpret_cast<const uint4*>(p));
+        return load16_row<false>(p, rem - o, vec);
+    };
+
+    const int64_t chunks = (kend - kbeg + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
+    const int64_t fast_chunks = ((vec_ok & 4) && n0 + 16 <= N) ? (kend - kbeg) / skinny_mma::CHUNK : 0;
+#pragma unroll 1
+    for (int64_t ch = warp; ch < chunks; ch += WARPS) {
+        const bool fast = ch < fast_chunks;  // warp-uniform
+        uint32_t bw[2][2][4];                // [row g / g+8][half c][word]
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+            const int64_t o = ch * skinny_mma::CHUNK + c * 64;
+            const uint4 v0 = fast ? load16_row<true>(pb + o, 16, true) : load16_row<true>(pb + o, ok_b0 ? rem - o : 0, vec);
+            const uint4 v1 = fast ? load16_row<true>(pb + 8 * ldb + o, 16, true)
+                                  : load16_row<true>(pb + 8 * ldb + o, ok_b1 ? rem - o : 0, vec);
+            bw[0][c][0] = v0.x; bw[0][c][1] = v0.y; bw[0][c][2] = v0.z; bw[0][c][3] = v0.w;
+            bw[1][c][0] = v1.x; bw[1][c][1] = v1.y; bw[1][c][2] = v1.z; bw[1][c][3] = v1.w;
+        }
+        // the MMA's A-row fragments travel with the B loads (one latency, not two)
+        uint4 av[NB][2];
+#pragma unroll
+        for (int c = 0; c < 2; ++c)
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+                const bool ok = nb * 8 + g < M;
+                av[nb][c] = load_a(ok ? nb * 8 + g : 0, ch * skinny_mma::CHUNK + c * 64, fast);
+                if (!ok) av[nb][c] = make_uint4(0, 0, 0, 0);
+            }
+        // listed words: a pair can clamp iff |b0 + b1| >= 129  <=>  unsigned(b0 + b1 + 128) > 256
+        uint32_t listed = 0;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    const uint32_t s0 = static_cast<uint32_t>(dp4a_ss(bw[r][c][q], 0x00000101u, 128));
+                    const uint32_t s1 = static_cast<uint32_t>(dp4a_ss(bw[r][c][q], 0x01010000u, 128));
+                    if (s0 > 256u || s1 > 256u) listed |= 1u << (r * 8 + c * 4 + q);
+                }
+        const int mine = __popc(listed);
+        const int total = __reduce_add_sync(0xffffffffu, mine);
+        if (total > QCAP) {
+            // ---- dense: the chunk's saturating sums for every A row, accumulated in registers
+            // (A-side pair masks: two LOPs per A word shared by both B rows, as in skinny_sat_kernel;
+            // an out-of-line version kept the sparse path's registers lower but ran 1.6x slower)
+            used_dense = true;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                if (m >= M) break;  // uniform
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint4 am = load_a(m, ch * skinny_mma::CHUNK + c * 64, fast);
+                    const uint32_t aw[4] = {am.x, am.y, am.z, am.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint32_t alo = aw[q] & 0x0000FFFFu, ahi = aw[q] & 0xFFFF0000u;
+                        dacc[0][m] = sat_word_add(alo, ahi, bw[0][c][q], dacc[0][m]);
+                        dacc[1][m] = sat_word_add(alo, ahi, bw[1][c][q], dacc[1][m]);
+                    }
+                }
+            }
+            continue;
+        }
+        // ---- sparse: exact MMAs on everything ...
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) {
+                const uint32_t aa[4] = {av[nb][c].x, av[nb][c].y, av[nb][c].z, av[nb][c].w};
+#pragma unroll
+                for (int j = 0; j < 2; ++j)
+                    mma_u8s8_m16n8k32(d[nb], bw[0][c][2 * j], bw[1][c][2 * j], bw[0][c][2 * j + 1], bw[1][c][2 * j + 1],
+                                      aa[2 * j], aa[2 * j + 1]);
+            }
+        }
+        if (total == 0) continue;
+        // ... then the listed words: queue them (exclusive scan of the lanes' counts) ...
+        int before = mine;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int up = __shfl_up_sync(0xffffffffu, before, o);
+            if (lane >= o) before += up;
+        }
+        int pos = before - mine;
+#pragma unroll
+        for (int r = 0; r < 2; ++r)
+#pragma unroll
+            for (int c = 0; c < 2; ++c)
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    if (listed & (1u << (r * 8 + c * 4 + q))) {
+                        // meta: K offset of the word inside the CTA's K range, B row of the tile
+                        const uint32_t koff = static_cast<uint32_t>(ch * skinny_mma::CHUNK + c * 64 + t * 16 + q * 4);
+                        my_queue[pos++] = make_uint2(bw[r][c][q], (koff << 4) | static_cast<uint32_t>(g + 8 * r));
+                    }
+        __syncwarp();
+        // ... and spread (word, A row) units over the lanes, four per lane and pass (loads first)
+        for (int base = 0; base < total * 16; base += 128) {
+            uint2 e[4];
+            uint32_t aw[4];
+            bool on[4];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int u = base + i * 32 + lane;
+                on[i] = u < total * 16 && (u & 15) < M;
+                e[i] = on[i] ? my_queue[u >> 4] : make_uint2(0, 0);
+                const int64_t kk = kbeg + (e[i].y >> 4);
+                const uint8_t* p = A + static_cast<int64_t>(u & 15) * lda + kk;
+                aw[i] = 0;
+                if (on[i]) {
+                    if (vec && kk + 4 <= kend) {
+                        aw[i] = __ldg(reinterpret_cast<const uint32_t*>(p));
+                    } else {
+                        for (int b4 = 0; b4 < 4; ++b4)
+                            if (kk + b4 < kend) aw[i] |= static_cast<uint32_t>(__ldg(p + b4)) << (8 * b4);
+                    }
+                }
+            }
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const int32_t p0 = dp4a_us(aw[i], e[i].x & 0x0000FFFFu, 0), p1 = dp4a_us(aw[i], e[i].x & 0xFFFF0000u, 0);
+                const int32_t fix = sat2_add(p0, p1, 0) - (p0 + p1);
+                if (on[i] && fix != 0) atomicAdd(&corr[(e[i].y & 15u) * MT + ((base + i * 32 + lane) & 15)], fix);
+            }
+        }
+        __syncwarp();
+    }
+
+    if (used_dense) {  // warp-uniform
+        if (lane == 0) *dense_used = 1;  // read after the block-wide barrier below
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            my_part[m] += dacc[0][m];
+            my_part[8 * MT + m] += dacc[1][m];
+        }
+    }
+    // this lane's MMA fragment into its own part cells: d[nb] = rows {g, g+8} x A rows nb*8 + 2t, +1
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        const int col = nb * 8 + t * 2;
+        my_part[col] += d[nb][0];
+        my_part[col + 1] += d[nb][1];
+        my_part[8 * MT + col] += d[nb][2];
+        my_part[8 * MT + col + 1] += d[nb][3];
+    }
+    __syncthreads();
+    for (int i = tid; i < 16 * MT; i += WARPS * 32) {
+        const int m = i / 16, row = i % 16;
+        uint32_t s = static_cast<uint32_t>(corr[row * MT + m]);
+        if (*dense_used) {
+#pragma unroll 8
+            for (int w = 0; w < WARPS * 4; ++w) s += static_cast<uint32_t>(part[(w * 16 + row) * MT + m]);
+        } else {
+            // MMA fragments only: A row m sits in K-phase plane (m % 8) / 2 of every warp
+#pragma unroll
+            for (int w = 0; w < WARPS; ++w)
+                s += static_cast<uint32_t>(part[((w * 4 + ((m & 7) >> 1)) * 16 + row) * MT + m]);
+        }
+        const int64_t n = n0 + row;
+        if (m < M && n < N) {
+            int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;
+            if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
+            else *dst = static_cast<int32_t>(s);
+        }
+    }
+}
+
+}  // namespace ngemm_dev

@@ -646,6 +646,57 @@ ngemm_status launch_skinny_sat_t(const uint8_t* a, int64_t lda, const int8_t* b,
     return launch_skinny_sat_w<MT, 32, false>(a, lda, b, ldb, c, ldc, m, n, k, (ks + 31) / 32, di, st, bt);
 }
 
+// Saturating tensor-core + sparse-fix variant (skinny_sathyb_kernel, 4 < M <= 16): one 16-row group
+// of B per CTA, 8 or 16 warps splitting K like the exact warp-MMA stream, a grid K split when
+// even 16 warps per row group leave SMs short of streaming warps.
+template <int MT, int WARPS>
+ngemm_status launch_skinny_sathyb_w(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                    int64_t ldc, int64_t m, int64_t n, int64_t k, int64_t splits, cudaStream_t st,
+                                    const Batch& bt) {
+    using S = skinny_sathyb::Smem<MT, WARPS>;
+    auto kern = skinny_sathyb_kernel<MT, WARPS>;
+    static std::once_flag once[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    ngemm_status s = NGEMM_OK;
+    // no shared-memory carveout preference: A is re-read through L1
+    if (S::TOTAL > 48 * 1024)
+        std::call_once(once[dev & 63], [&] {
+            if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, S::TOTAL) != cudaSuccess)
+                s = fail(NGEMM_ERR_CUDA, "cudaFuncSetAttribute(skinny_sathyb) failed");
+        });
+    if (s != NGEMM_OK) return s;
+    const int64_t groups = (n + 15) / 16;
+    const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
+    splits = (k + k_range - 1) / k_range;
+    for (int z = 0; z < bt.count && splits > 1; ++z) {
+        ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, st);
+        if (zs != NGEMM_OK) return zs;
+    }
+    const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
+    NG_LAUNCH(kern, dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
+              dim3(WARPS * 32), S::TOTAL, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
+              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
+    return NGEMM_OK;
+}
+
+template <int MT>
+ngemm_status launch_skinny_sathyb_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
+                                    int64_t ldc, int64_t m, int64_t n, int64_t k, const DevInfo& di, cudaStream_t st,
+                                    const Batch& bt = Batch()) {
+    const int64_t groups = (n + 15) / 16 * bt.count;
+    const int64_t chunks = (k + skinny_mma::CHUNK - 1) / skinny_mma::CHUNK;
+    const int64_t warps_target = static_cast<int64_t>(di.sms) * 32;
+    const int64_t ks = std::max<int64_t>(1, std::min<int64_t>(chunks, (warps_target + groups - 1) / groups));
+    int64_t splits = 1;
+    if (opt(O_SKINNY_SPLITS) > 0) splits = opt(O_SKINNY_SPLITS);
+    int64_t ks_use = std::min<int64_t>(ks, 16);
+    if (opt(O_SKINNY_WARPS) > 0) ks_use = opt(O_SKINNY_WARPS);
+    if (splits == 1 && ks_use < ks && opt(O_SKINNY_WARPS) <= 0) splits = (ks + ks_use - 1) / ks_use;
+    if (ks_use <= 8) return launch_skinny_sathyb_w<MT, 8>(a, lda, b, ldb, c, ldc, m, n, k, splits, st, bt);
+    return launch_skinny_sathyb_w<MT, 16>(a, lda, b, ldb, c, ldc, m, n, k, splits, st, bt);
+}
+
 // Lanes-own-rows variant (skinny_rows_kernel): 32-row tiles of B x K splits.
 template <int MODE, int MT>
 ngemm_status launch_skinny_rows_t(const uint8_t* a, int64_t lda, const int8_t* b, int64_t ldb, int32_t* c,
@@ -691,7 +742,11 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
     // ~1 us more for TMEM/mbarrier/cluster setup); saturating -> the dp4a load stream (4),
     // which since the pack-saturate step also beats the broadcast kernel (1) on every
     // M > 4, N < 2048 shape (profiles/sweep_r1_skinny_sat_variants.log).
-    int variant = mode == NGEMM_SAT_EXACT ? 3 : 4;
+    // Saturating, 8 < M <= 16: warp MMAs + sparse fix (5) — 1.3-1.5x faster than the dp4a stream on
+    // weight-like B (config 2's sigma = 32: ~0.4 % of the pairs can clamp), 1.3-1.5x slower when
+    // most pairs can (uniform int8 B takes its dense branch); NGEMM_SKINNY_VARIANT=4 or a tune-store
+    // entry selects the dp4a stream (profiles/r2/skinny_sathyb_r2.log).
+    int variant = mode == NGEMM_SAT_EXACT ? 3 : (m > 8 ? 5 : 4);
     if (opt(O_SKINNY_VARIANT) >= 0) variant = opt(O_SKINNY_VARIANT);  // experiments
     if (t_force.skinny_variant >= 0) variant = t_force.skinny_variant;
     if (variant == 2 && mode == NGEMM_SAT_EXACT) return launch_tc_skinny(a, lda, b, ldb, c, ldc, m, n, k, di, st);
@@ -701,6 +756,9 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
         if (m <= 8) return launch_skinny_sat_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
         return launch_skinny_sat_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     }
+    if (variant == 5 && mode != NGEMM_SAT_EXACT)
+        return m <= 8 ? launch_skinny_sathyb_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
+                      : launch_skinny_sathyb_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
     if (variant == 3 && mode == NGEMM_SAT_EXACT)
         return m <= 8 ? launch_skinny_mma_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st)
                       : launch_skinny_mma_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st);
@@ -1156,7 +1214,8 @@ ngemm_status run_gemm_batched(const uint8_t* a, int64_t lda, int64_t sa, const i
         if (m <= 1) return launch_skinny_sat_t<1>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
         if (m <= 4) return launch_skinny_sat_t<4>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
         if (m <= 8) return launch_skinny_sat_t<8>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
-        return launch_skinny_sat_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+        if (opt(O_SKINNY_VARIANT) == 4) return launch_skinny_sat_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
+        return launch_skinny_sathyb_t<16>(a, lda, b, ldb, c, ldc, m, n, k, di, st, bt);
     }
     for (int64_t z = 0; z < count; ++z) {
         s = run_gemm(a + z * sa, lda, b + z * sb, ldb, c + z * sc, ldc, m, n, k, mode, NGEMM_KERNEL_AUTO, st);
@@ -2023,8 +2082,8 @@ ngemm_status ngemm_cuda_tune(int64_t m, int64_t n, int64_t k, int sat_mode, int 
 
     std::vector<Choice> cands;
     if (m <= kSkinnyMaxM) {
-        for (int v = 0; v < 5; ++v) {
-            if (sat_mode == NGEMM_SAT_EXACT ? v == 4 : (v == 2 || v == 3)) continue;
+        for (int v = 0; v < 6; ++v) {
+            if (sat_mode == NGEMM_SAT_EXACT ? v >= 4 : (v == 2 || v == 3)) continue;
             Choice c;
             c.kernel = NGEMM_KERNEL_SKINNY;
             c.skinny_variant = v;

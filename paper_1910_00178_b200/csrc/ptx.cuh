@@ -38,6 +38,22 @@ __device__ __forceinline__ int32_t sat_word_add(uint32_t alo, uint32_t ahi, uint
     return r;
 }
 
+// s8 x s8 dot product of 4 byte lanes plus accumulator (IDP.4A.S8.S8).
+__device__ __forceinline__ int32_t dp4a_ss(uint32_t a, uint32_t b, int32_t c) {
+    int32_t d;
+    asm("dp4a.s32.s32 %0, %1, %2, %3;" : "=r"(d) : "r"(a), "r"(b), "r"(c));
+    return d;
+}
+
+// acc += sat16(p0) + sat16(p1) (cvt.pack.sat.s16.s32 clamps both, dp2a adds the halves).
+__device__ __forceinline__ int32_t sat2_add(int32_t p0, int32_t p1, int32_t acc) {
+    uint32_t packed;
+    asm("cvt.pack.sat.s16.s32 %0, %1, %2;" : "=r"(packed) : "r"(p1), "r"(p0));
+    int32_t r;
+    asm("dp2a.lo.s32.s32 %0, %1, %2, %3;" : "=r"(r) : "r"(packed), "r"(0x0101), "r"(acc));
+    return r;
+}
+
 // a * b + c on the FMA pipe (IMAD), wrapping mod 2^32.
 __device__ __forceinline__ int32_t imad_u32(int32_t a, int32_t b, int32_t c) {
     int32_t d;

@@ -409,11 +409,12 @@ def test_tcgen05_tail_split(cuda, oracle, cfg, knobs):
     assert (out.cpu().numpy() == y).all(), int((out.cpu().numpy() != y).sum())
 
 
-@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4"])
+@pytest.mark.parametrize("variant", ["0", "1", "2", "3", "4", "5"])
 def test_skinny_variants(cuda, oracle, golden, variant, knobs):
     """Skinny (M <= 16) variants: 0 warp-butterfly dp4a, 1 lanes-own-rows dp4a (broadcast A),
     2 tensor-core swap-AB, 3 warp-MMA load stream (2 and 3: exact mode only; sat falls back
-    to 1), 4 dp4a load stream (sat) — all bit-exact."""
+    to 1), 4 dp4a load stream (sat), 5 warp-MMA + sparse fix (sat; exact falls back to 1) — all
+    bit-exact."""
     knobs.set("SKINNY_VARIANT", variant)
     for c in golden["config2"]:
         a = oracle.mat_random_u8(c["m"], c["k"], 0)
@@ -426,6 +427,55 @@ def test_skinny_variants(cuda, oracle, golden, variant, knobs):
         b = oracle.mat_random_i8(n, k, n)
         for mode in (EXACT, SAT):
             assert (dev_gemm(a, b, mode, "skinny", lda, ldb, ldc) == oracle.gemm(a, b, mode)).all(), (variant, m, n, k)
+
+
+def test_skinny_sat_tensor_core_fix(cuda, oracle, knobs):
+    """skinny_sathyb_kernel (variant 5): exact warp MMAs plus the sparse correction of the pairs
+    with |b0 + b1| >= 129, and its dense branch (> 128 listed words per warp chunk).  Threshold
+    pairs (64,65), (65,64), (-64,-65), (64,64), (127,-128), saturated pairs (127,127),
+    (-128,-128) sprinkled into a weight-like B (sparse branch), uniform and all-extreme B (dense
+    branch), A all 255 / alternating / uniform, ragged K and N, unaligned leading dimensions, K
+    splits over the grid, 8 and 16 warps."""
+    import numpy as np
+    knobs.set("SKINNY_VARIANT", "5")
+    rng = np.random.default_rng(11)
+    special = np.array([[64, 65], [65, 64], [-64, -65], [-65, -64], [64, 64], [-64, -64], [127, -128], [-128, 127],
+                        [127, 127], [-128, -128], [127, 2], [-128, -1], [0, 127], [-128, 0], [100, 29], [-100, -29]], np.int8)
+    shapes = [(16, 4096, 1024, None, None, None), (9, 768, 3072, None, None, None), (16, 130, 1001, 1008, 1003, 132),
+              (5, 77, 255, None, None, None), (16, 48, 16384, None, None, None), (12, 3072, 768, None, None, None),
+              (8, 1000, 130, 144, 131, 1000), (16, 16, 127, None, None, None), (3, 4096, 1024, None, None, None)]
+    for (m, n, k, lda, ldb, ldc) in shapes:
+        for bkind in ("normal", "uniform", "max", "min", "alt"):
+            if bkind == "normal":
+                b = oracle.mat_normal_i8(n, k, n + 5, 32.0).copy()
+                # sprinkle threshold / saturating pairs at even-aligned positions
+                for _ in range(max(4, n * k // 2000)):
+                    r, j = int(rng.integers(0, n)), int(rng.integers(0, max(1, k // 2)))
+                    if 2 * j + 1 < k:
+                        b[r, 2 * j:2 * j + 2] = special[int(rng.integers(0, len(special)))]
+            elif bkind == "uniform":
+                b = oracle.mat_random_i8(n, k, n + 6)
+            else:
+                b = np.full((n, k), 127 if bkind == "max" else -128, np.int8)
+                if bkind == "alt":
+                    b[:, 1::2] = 127
+            for akind in ("uniform", "max", "alt"):
+                if akind == "uniform":
+                    a = oracle.mat_random_u8(m, k, m + 3)
+                else:
+                    a = np.full((m, k), 255, np.uint8)
+                    if akind == "alt":
+                        a[:, 0::2] = 0
+                ref = oracle.gemm(a, b, SAT)
+                for warps in ("-1", "8", "16"):
+                    knobs.set("SKINNY_WARPS", warps)
+                    got = dev_gemm(a, b, SAT, "skinny", lda, ldb, ldc)
+                    assert (got == ref).all(), (m, n, k, bkind, akind, warps, int((got != ref).sum()))
+                knobs.set("SKINNY_WARPS", "-1")
+                knobs.set("SKINNY_SPLITS", "3")
+                got = dev_gemm(a, b, SAT, "skinny", lda, ldb, ldc)
+                knobs.set("SKINNY_SPLITS", "-1")
+                assert (got == ref).all(), (m, n, k, bkind, akind, "splits", int((got != ref).sum()))
 
 
 @pytest.mark.parametrize("hybrid", ["1", "-1"])
