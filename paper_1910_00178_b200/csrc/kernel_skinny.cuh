@@ -435,12 +435,33 @@ __global__ void __launch_bounds__(WARPS * 32)
     }
     __syncthreads();
     SKINNY_TRACE_AT(3);
+    // accumulate == 2 (RG = 1): the grid's K splits of a row group form one thread-block cluster
+    // along y; every rank publishes its 16 x MT partial sums in shared memory and rank r adds up and
+    // stores the outputs i with i % splits == r through DSMEM — no zeroing pass, no atomics
+    __shared__ int32_t xsum[RG == 1 ? 16 * MT : 1];
+    const bool xred = RG == 1 && accumulate == 2;
+    const uint32_t nsplit = gridDim.y, xrank = blockIdx.y;
+    if (xred) {
+        for (int i = tid; i < 16 * MT; i += WARPS * 32) {
+            const int m = i / 16, row = i % 16;
+            uint32_t s = 0;
+#pragma unroll
+            for (int q = 0; q < KS; ++q) s += static_cast<uint32_t>(red[(q * 16 + row) * MT + m]);
+            xsum[i] = static_cast<int32_t>(s);
+        }
+        cluster_sync();
+    }
     for (int i = tid; i < RG * 16 * MT; i += WARPS * 32) {
         const int m = i / (RG * 16), rr = i % (RG * 16);  // consecutive threads -> consecutive n
         const int r_g = rr / 16, row = rr % 16;
         uint32_t s = 0;
+        if (xred) {
+            if (static_cast<uint32_t>(i) % nsplit != xrank) continue;
+            for (uint32_t q = 0; q < nsplit; ++q) s += dsmem_ld_u32(smem_u32(&xsum[i]), q);
+        } else {
 #pragma unroll
-        for (int q = 0; q < KS; ++q) s += static_cast<uint32_t>(red[((r_g * KS + q) * 16 + row) * MT + m]);
+            for (int q = 0; q < KS; ++q) s += static_cast<uint32_t>(red[((r_g * KS + q) * 16 + row) * MT + m]);
+        }
         const int64_t n = (static_cast<int64_t>(blockIdx.x) * RG + r_g) * 16 + row;
         if (m < M && n < N) {
             if (rq.out != nullptr) {  // fused requantisation (single K split only)
@@ -448,10 +469,11 @@ __global__ void __launch_bounds__(WARPS * 32)
                 continue;
             }
             int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;
-            if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
+            if (accumulate == 1) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
             else *dst = static_cast<int32_t>(s);
         }
     }
+    if (xred) cluster_sync();  // peers may still be reading this CTA's partial sums
     SKINNY_TRACE_AT(4);
     SKINNY_TRACE_END();
 }
@@ -913,8 +935,23 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
         my_part[8 * MT + col + 1] += d[nb][3];
     }
     __syncthreads();
+    // accumulate == 2: K splits reduced across a thread-block cluster through DSMEM, as in
+    // skinny_mma_kernel (xsum aliases the queue, which is no longer in use)
+    int32_t* xsum = reinterpret_cast<int32_t*>(queue);
+    const bool xred = accumulate == 2;
+    const uint32_t nsplit = gridDim.y, xrank = blockIdx.y;
+    for (int pass = 0; pass < (xred ? 2 : 1); ++pass) {
+    if (xred && pass == 1) cluster_sync();
     for (int i = tid; i < 16 * MT; i += WARPS * 32) {
         const int m = i / 16, row = i % 16;
+        if (xred && pass == 1) {
+            if (static_cast<uint32_t>(i) % nsplit != xrank) continue;
+            uint32_t t2 = 0;
+            for (uint32_t q = 0; q < nsplit; ++q) t2 += dsmem_ld_u32(smem_u32(&xsum[i]), q);
+            const int64_t n2 = n0 + row;
+            if (m < M && n2 < N) C[static_cast<int64_t>(m) * ldc + n2] = static_cast<int32_t>(t2);
+            continue;
+        }
         uint32_t s = static_cast<uint32_t>(corr[row * MT + m]);
         if (*dense_used) {
 #pragma unroll 8
@@ -925,13 +962,19 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
             for (int w = 0; w < WARPS; ++w)
                 s += static_cast<uint32_t>(part[((w * 4 + ((m & 7) >> 1)) * 16 + row) * MT + m]);
         }
+        if (xred) {
+            xsum[i] = static_cast<int32_t>(s);
+            continue;
+        }
         const int64_t n = n0 + row;
         if (m < M && n < N) {
             int32_t* dst = C + static_cast<int64_t>(m) * ldc + n;
-            if (accumulate) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
+            if (accumulate == 1) atomicAdd(reinterpret_cast<unsigned int*>(dst), s);
             else *dst = static_cast<int32_t>(s);
         }
     }
+    }
+    if (xred) cluster_sync();  // peers may still be reading this CTA's partial sums
 }
 
 }  // namespace ngemm_dev

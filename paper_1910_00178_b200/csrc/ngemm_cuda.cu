@@ -117,7 +117,7 @@ DevInfo dev_info(int dev) {
 enum Opt : int {
     O_PDL, O_L2_PREFETCH, O_SKINNY_FAST, O_SKINNY_SPLITS, O_SKINNY_RG, O_SKINNY_WARPS, O_SKINNY_VARIANT,
     O_TC_QUAD, O_TC_CFG, O_TC_SPLITS, O_TC_DIRECT, O_TC_PREISSUE, O_TC_L2HINT, O_TC_GROUP_M, O_TC_DBG,
-    O_SAT_HYBRID, O_SATFIX_SKIP, O_I16_PATH, O_REQUANT_UNFUSED, O_TC_SCHED, O_N
+    O_SAT_HYBRID, O_SATFIX_SKIP, O_I16_PATH, O_REQUANT_UNFUSED, O_TC_SCHED, O_SKINNY_XRED, O_N
 };
 struct OptDef {
     const char* name;
@@ -128,6 +128,7 @@ constexpr OptDef kOpts[O_N] = {
     {"SKINNY_WARPS", -1}, {"SKINNY_VARIANT", -1}, {"TC_QUAD", 0}, {"TC_CFG", -1}, {"TC_SPLITS", -1},
     {"TC_DIRECT", 0}, {"TC_PREISSUE", 0}, {"TC_L2HINT", 7}, {"TC_GROUP_M", -1}, {"TC_DBG", 0},
     {"SAT_HYBRID", -1}, {"SATFIX_SKIP", 0}, {"I16_PATH", -1}, {"REQUANT_UNFUSED", 0}, {"TC_SCHED", -1},
+    {"SKINNY_XRED", 1},
 };
 std::atomic<int> g_opt[O_N];
 std::once_flag g_opt_once;
@@ -531,15 +532,21 @@ ngemm_status launch_skinny_mma_w(const uint8_t* a, int64_t lda, const int8_t* b,
     if (rq.out != nullptr) splits = 1;  // the requantised value needs the whole K sum
     const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
     splits = (k + k_range - 1) / k_range;
-    for (int z = 0; z < bt.count && splits > 1; ++z) {
+    // Two K splits of one row group run as a 2-CTA cluster and meet through DSMEM (no zeroing pass,
+    // no atomics: 16x768x3072 4.95 -> 4.35 us); 4- and 8-CTA clusters schedule too slowly (16x256x16384
+    // 8.6 vs 5.1 us, profiles/r2/skinny_xred_ab_r2.log), so more splits wrap-add into a zeroed C.
+    // SKINNY_XRED=2 forces the cluster for up to 8 splits (tests).
+    const bool xred = RG == 1 && splits > 1 && (splits == 2 || (splits <= 8 && opt(O_SKINNY_XRED) == 2)) &&
+                      opt(O_SKINNY_XRED) != 0;
+    for (int z = 0; z < bt.count && splits > 1 && !xred; ++z) {
         ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
     NG_LAUNCH(skinny_mma_kernel<MT, RG, WARPS>,
               dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
-              dim3(WARPS * 32), 0, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
-              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc, rq);
+              dim3(WARPS * 32), 0, st, 1, xred ? static_cast<unsigned>(splits) : 1u, a, lda, b, ldb, c, ldc,
+              static_cast<int>(m), n, k, k_range, vec, xred ? 2 : (splits > 1 ? 1 : 0), bt.sa, bt.sb, bt.sc, rq);
     return NGEMM_OK;
 }
 
@@ -669,14 +676,16 @@ ngemm_status launch_skinny_sathyb_w(const uint8_t* a, int64_t lda, const int8_t*
     const int64_t groups = (n + 15) / 16;
     const int64_t k_range = round_up((k + splits - 1) / splits, skinny_mma::CHUNK);
     splits = (k + k_range - 1) / k_range;
-    for (int z = 0; z < bt.count && splits > 1; ++z) {
+    // cluster reduction for two splits, as in the exact stream
+    const bool xred = splits > 1 && (splits == 2 || (splits <= 8 && opt(O_SKINNY_XRED) == 2)) && opt(O_SKINNY_XRED) != 0;
+    for (int z = 0; z < bt.count && splits > 1 && !xred; ++z) {
         ngemm_status zs = zero_c(c + z * bt.sc, ldc, m, n, st);
         if (zs != NGEMM_OK) return zs;
     }
     const int vec = skinny_vec_flags(a, lda, b, ldb, bt);
     NG_LAUNCH(kern, dim3(static_cast<unsigned>(groups), static_cast<unsigned>(splits), static_cast<unsigned>(bt.count)),
-              dim3(WARPS * 32), S::TOTAL, st, 1, 1, a, lda, b, ldb, c, ldc, static_cast<int>(m), n, k, k_range, vec,
-              splits > 1 ? 1 : 0, bt.sa, bt.sb, bt.sc);
+              dim3(WARPS * 32), S::TOTAL, st, 1, xred ? static_cast<unsigned>(splits) : 1u, a, lda, b, ldb, c, ldc,
+              static_cast<int>(m), n, k, k_range, vec, xred ? 2 : (splits > 1 ? 1 : 0), bt.sa, bt.sb, bt.sc);
     return NGEMM_OK;
 }
 

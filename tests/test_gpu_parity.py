@@ -429,6 +429,32 @@ def test_skinny_variants(cuda, oracle, golden, variant, knobs):
             assert (dev_gemm(a, b, mode, "skinny", lda, ldb, ldc) == oracle.gemm(a, b, mode)).all(), (variant, m, n, k)
 
 
+def test_skinny_cluster_k_splits(cuda, oracle, knobs):
+    """Grid K splits of the skinny load streams (exact warp-MMA stream, saturating MMA + fix): two
+    splits (up to 8 with SKINNY_XRED=2) form a thread-block cluster and meet through distributed
+    shared memory (no zeroed C, no atomics); more splits, or SKINNY_XRED=0, wrap-add into a zeroed C.  Deep-K / narrow-N
+    shapes where the planner splits on its own, and forced split counts, ragged K included."""
+    for (m, n, k, lda, ldb, ldc) in ((16, 768, 3072, None, None, None), (16, 48, 16384, None, None, None),
+                                     (9, 256, 16384, None, None, None), (16, 130, 4097, 4112, 4100, 131),
+                                     (5, 64, 1000, None, None, None)):
+        a = oracle.mat_random_u8(m, k, m + 21)
+        b = oracle.mat_normal_i8(n, k, n + 22, 32.0)
+        for mode in (EXACT, SAT):
+            ref = oracle.gemm(a, b, mode)
+            for xred in ("2", "1", "0"):  # 2: clusters for up to 8 splits, 1: default (two splits), 0: never
+                knobs.set("SKINNY_XRED", xred)
+                for splits in ("-1", "2", "3", "5", "8", "11"):
+                    knobs.set("SKINNY_SPLITS", splits)
+                    got = dev_gemm(a, b, mode, "skinny", lda, ldb, ldc)
+                    assert (got == ref).all(), (m, n, k, mode, xred, splits, int((got != ref).sum()))
+    knobs.set("SKINNY_VARIANT", "5")  # the MMA + fix stream for M <= 8 too
+    a = oracle.mat_random_u8(7, 2048, 3)
+    b = oracle.mat_normal_i8(96, 2048, 4, 32.0)
+    for splits in ("2", "4"):
+        knobs.set("SKINNY_SPLITS", splits)
+        assert (dev_gemm(a, b, SAT, "skinny") == oracle.gemm(a, b, SAT)).all(), splits
+
+
 def test_skinny_sat_tensor_core_fix(cuda, oracle, knobs):
     """skinny_sathyb_kernel (variant 5): exact warp MMAs plus the sparse correction of the pairs
     with |b0 + b1| >= 129, and its dense branch (> 128 listed words per warp chunk).  Threshold
