@@ -291,7 +291,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1)
 #pragma unroll
                     for (int h = 0; h < BN / S::MMA_N; ++h) {
                         // BN = 512: MMA h reads rows [128h, 128h + 128) of each CTA's B slab (this
-                        // CTA's 256 rows of B) and accumulates into TMEM columns [256h, 256h + 256)
+                        // CTA's 256 rows of B) and accumulates into TMEM columns [256h, 256h + 256).
+                        // All K steps of a stage go into one accumulator before the other: issuing
+                        // the two accumulators' MMAs alternately (so that they could share the A
+                        // collector) measured 15 % slower (profiles/r2/collector_kmajor_ab_r2.log)
 #pragma unroll
                         for (int k = 0; k < tc::BK / tc::UMMA_K; ++k) {
                             if (map.dbg & 2) break;
