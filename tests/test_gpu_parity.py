@@ -358,6 +358,67 @@ def test_config5_full_size(cuda, oracle, golden, mode):
         assert torch.equal(lhs, rhs)
 
 
+def test_dispatcher_fuzz_auto(cuda, oracle):
+    """AUTO dispatch over 160 seeded random problems drawn around every planner boundary (skinny
+    M <= 16 with narrow / wide N and shallow / deep K, the saturating MMA + fix kernel's M > 8,
+    cluster and atomic K splits, 1-CTA / pair / split-K tcgen05 shapes, the SIMT / hybrid size
+    rule), ragged sizes and padded leading dimensions, both SatModes, weight-like and uniform B —
+    every result bit-exact against the oracle."""
+    rng = np.random.default_rng(20251021)
+    def pick(lo, hi):
+        return int(np.exp(rng.uniform(np.log(lo), np.log(hi))))
+    for it in range(160):
+        kind = it % 4
+        if kind == 0:    # skinny
+            m, n, k = int(rng.integers(1, 17)), pick(1, 6000), pick(1, 20000)
+        elif kind == 1:  # small / medium
+            m, n, k = pick(17, 700), pick(1, 1500), pick(1, 3000)
+        elif kind == 2:  # wide or deep
+            m, n, k = pick(17, 300), pick(500, 5000), pick(500, 9000)
+        else:            # around the hybrid's size rule (M >= 256, >= 1e9 MACs)
+            m, n, k = pick(200, 1200), pick(700, 1500), pick(700, 1500)
+        while 2.0 * m * n * k > 6e9:
+            k = max(1, k // 2)
+        pad = int(rng.integers(0, 3))
+        lda = k + (0 if pad == 0 else int(rng.integers(1, 40)))
+        ldb = k + (0 if pad == 0 else int(rng.integers(1, 40)))
+        ldc = n + (0 if pad != 2 else int(rng.integers(1, 9)))
+        a = oracle.mat_random_u8(m, k, 1000 + it)
+        b = oracle.mat_normal_i8(n, k, 2000 + it, 32.0) if it % 3 else oracle.mat_random_i8(n, k, 2000 + it)
+        for mode in (EXACT, SAT):
+            got = dev_gemm(a, b, mode, "auto", lda, ldb, ldc)
+            assert (got == oracle.gemm(a, b, mode)).all(), (it, m, n, k, lda, ldb, ldc, mode)
+
+
+@pytest.mark.slow
+def test_pair512_tiles_through_auto_ragged(cuda, oracle):
+    """A ragged deep-K problem that AUTO runs on the 256 x 512 pair tiles (K >= 8192, >= 4 waves):
+    4100 x 8300 x 8200, partial tiles on M and N, a K tail inside a 128-byte slab, padded ldc.  Eight row
+    blocks (first / last tile rows and random ones) bit-exact against the oracle, and 16 Freivalds
+    rounds over the whole C (exact in float64: |C| < 2^31, x < 16, sums < 2^53)."""
+    import torch
+    m, n, k = 4100, 8300, 8200
+    a = oracle.mat_random_u8(m, k, 31)
+    b = oracle.mat_random_i8(n, k, 32)
+    da = torch.zeros((m, 8208), dtype=torch.uint8, device="cuda")
+    db = torch.zeros((n, 8208), dtype=torch.int8, device="cuda")
+    da[:, :k] = torch.from_numpy(a)
+    db[:, :k] = torch.from_numpy(b)
+    frame = torch.full((m, 8304), 0x5A5A5A5A, dtype=torch.int32, device="cuda")
+    dc = frame[:, :n]
+    api.gemm_device(da[:, :k], db[:, :k], dc, mode=EXACT)
+    torch.cuda.synchronize()
+    assert (frame[:, n:] == 0x5A5A5A5A).all()
+    for r0 in (0, 192, 2048 - 32, 4100 - 64, 1000, 3333, 3840, 4032):
+        got = dc[r0:r0 + 64].cpu().numpy()
+        assert (got == oracle.gemm(np.ascontiguousarray(a[r0:r0 + 64]), b, EXACT)).all(), r0
+    gen = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randint(0, 16, (n, 16), device="cuda", generator=gen).to(torch.float64)
+    lhs = dc.to(torch.float64) @ x
+    rhs = da[:, :k].to(torch.float64) @ (db[:, :k].to(torch.float64).t() @ x)
+    assert torch.equal(lhs, rhs)
+
+
 @pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4, 5, 6, 7, 8, 9])
 def test_tcgen05_every_tile_config_and_split(cuda, oracle, cfg, knobs):
     """Each tcgen05 tile configuration (pair 256x256, 1-CTA 128x256/128/64, the 4-CTA and 2-CTA
