@@ -740,7 +740,9 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
     int32_t* part = reinterpret_cast<int32_t*>(sathyb_smem);
     uint2* queue = reinterpret_cast<uint2*>(sathyb_smem + S::PART);
     int32_t* corr = reinterpret_cast<int32_t*>(sathyb_smem + S::PART + S::QUEUE);
-    int* dense_used = reinterpret_cast<int*>(sathyb_smem + S::PART + S::QUEUE + S::CORR);
+    // bit w set: warp w took the dense path and wrote all of its part cells (else only its MMA
+    // fragment's cells are valid)
+    unsigned* dense_mask = reinterpret_cast<unsigned*>(sathyb_smem + S::PART + S::QUEUE + S::CORR);
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int g = lane >> 2, t = lane & 3;
     pdl_launch_dependents();
@@ -762,10 +764,8 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
     }
     // this lane's private cells part[warp][t][g + 8r][m], and the shared corrections
     int32_t* my_part = part + ((warp * 4 + t) * 16 + g) * MT;
-#pragma unroll
-    for (int m = 0; m < MT; ++m) my_part[m] = my_part[8 * MT + m] = 0;
     for (int i = tid; i < 16 * MT; i += WARPS * 32) corr[i] = 0;
-    if (tid == 0) *dense_used = 0;
+    if (tid == 0) *dense_mask = 0;
     __syncthreads();
     pdl_wait();
     const uint8_t* Bu = reinterpret_cast<const uint8_t*>(B);
@@ -773,7 +773,18 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
     const int64_t kt = kbeg + t * 16;
     const int64_t rem = kend - kt;
     const uint8_t* pb = Bu + (n0 + g) * ldb + kt;
+    const uint8_t* pb8 = pb + 8 * ldb;
     const bool ok_b0 = n0 + g < N, ok_b1 = n0 + g + 8 < N;
+    const uint8_t* pa_frag[NB];  // A rows nb*8 + g (row 0 stands in for rows past M; zeroed by a_ok)
+    bool a_ok[NB];
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb) {
+        a_ok[nb] = nb * 8 + g < M;
+        pa_frag[nb] = A + static_cast<int64_t>(a_ok[nb] ? nb * 8 + g : 0) * lda + kt;
+    }
+    // flush: lane l always handles A row l % 16 (units are entry * 16 + row, 32 lanes per step)
+    const uint8_t* pa_fix = A + static_cast<int64_t>(lane & 15) * lda + kbeg;
+    const bool fix_row_ok = (lane & 15) < M;
     uint2* my_queue = queue + warp * QCAP;
 
     int32_t d[NB][4];
@@ -797,25 +808,35 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
     for (int64_t ch = warp; ch < chunks; ch += WARPS) {
         const bool fast = ch < fast_chunks;  // warp-uniform
         uint32_t bw[2][2][4];                // [row g / g+8][half c][word]
+        uint4 av[NB][2];                     // the MMA's A-row fragments travel with the B loads
+        const uint32_t o0 = static_cast<uint32_t>(ch) * skinny_mma::CHUNK;
+        if (fast) {
+            // whole chunk in range and 16-byte aligned: eight plain vector loads
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-            const int64_t o = ch * skinny_mma::CHUNK + c * 64;
-            const uint4 v0 = fast ? load16_row<true>(pb + o, 16, true) : load16_row<true>(pb + o, ok_b0 ? rem - o : 0, vec);
-            const uint4 v1 = fast ? load16_row<true>(pb + 8 * ldb + o, 16, true)
-                                  : load16_row<true>(pb + 8 * ldb + o, ok_b1 ? rem - o : 0, vec);
-            bw[0][c][0] = v0.x; bw[0][c][1] = v0.y; bw[0][c][2] = v0.z; bw[0][c][3] = v0.w;
-            bw[1][c][0] = v1.x; bw[1][c][1] = v1.y; bw[1][c][2] = v1.z; bw[1][c][3] = v1.w;
-        }
-        // the MMA's A-row fragments travel with the B loads (one latency, not two)
-        uint4 av[NB][2];
+            for (int c = 0; c < 2; ++c) {
+                const uint4 v0 = load16_row<true>(pb + o0 + c * 64, 16, true);
+                const uint4 v1 = load16_row<true>(pb8 + o0 + c * 64, 16, true);
+                bw[0][c][0] = v0.x; bw[0][c][1] = v0.y; bw[0][c][2] = v0.z; bw[0][c][3] = v0.w;
+                bw[1][c][0] = v1.x; bw[1][c][1] = v1.y; bw[1][c][2] = v1.z; bw[1][c][3] = v1.w;
 #pragma unroll
-        for (int c = 0; c < 2; ++c)
-#pragma unroll
-            for (int nb = 0; nb < NB; ++nb) {
-                const bool ok = nb * 8 + g < M;
-                av[nb][c] = load_a(ok ? nb * 8 + g : 0, ch * skinny_mma::CHUNK + c * 64, fast);
-                if (!ok) av[nb][c] = make_uint4(0, 0, 0, 0);
+                for (int nb = 0; nb < NB; ++nb) {
+                    const uint4 v = __ldg(reinterpret_cast<const uint4*>(pa_frag[nb] + o0 + c * 64));
+                    av[nb][c] = a_ok[nb] ? v : make_uint4(0, 0, 0, 0);
+                }
             }
+        } else {
+#pragma unroll
+            for (int c = 0; c < 2; ++c) {
+                const int64_t o = static_cast<int64_t>(o0) + c * 64;
+                const uint4 v0 = load16_row<true>(pb + o, ok_b0 ? rem - o : 0, vec);
+                const uint4 v1 = load16_row<true>(pb8 + o, ok_b1 ? rem - o : 0, vec);
+                bw[0][c][0] = v0.x; bw[0][c][1] = v0.y; bw[0][c][2] = v0.z; bw[0][c][3] = v0.w;
+                bw[1][c][0] = v1.x; bw[1][c][1] = v1.y; bw[1][c][2] = v1.z; bw[1][c][3] = v1.w;
+#pragma unroll
+                for (int nb = 0; nb < NB; ++nb)
+                    av[nb][c] = load16_row<false>(pa_frag[nb] + o, a_ok[nb] ? rem - o : 0, vec);
+            }
+        }
         // listed words: a pair can clamp iff |b0 + b1| >= 129  <=>  unsigned(b0 + b1 + 128) > 256
         uint32_t listed = 0;
 #pragma unroll
@@ -865,74 +886,82 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
             }
         }
         if (total == 0) continue;
-        // ... then the listed words: queue them (exclusive scan of the lanes' counts) ...
-        int before = mine;
+        // ... then the listed words: queue them (exclusive scan of the lanes' counts; a lane has
+        // none or one or two, so a short loop over its set bits with the word picked by a select
+        // tree beats sixteen predicated stores) ...
+        int pos = mine;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
-            const int up = __shfl_up_sync(0xffffffffu, before, o);
-            if (lane >= o) before += up;
+            const int up = __shfl_up_sync(0xffffffffu, pos, o);
+            if (lane >= o) pos += up;
         }
-        int pos = before - mine;
+        pos -= mine;
+        for (uint32_t rest = listed; rest != 0; rest &= rest - 1) {
+            const int i = __ffs(rest) - 1;  // (r * 8 + c * 4 + q)
+            uint32_t w = bw[0][0][0];
 #pragma unroll
-        for (int r = 0; r < 2; ++r)
-#pragma unroll
-            for (int c = 0; c < 2; ++c)
-#pragma unroll
-                for (int q = 0; q < 4; ++q)
-                    if (listed & (1u << (r * 8 + c * 4 + q))) {
-                        // meta: K offset of the word inside the CTA's K range, B row of the tile
-                        const uint32_t koff = static_cast<uint32_t>(ch * skinny_mma::CHUNK + c * 64 + t * 16 + q * 4);
-                        my_queue[pos++] = make_uint2(bw[r][c][q], (koff << 4) | static_cast<uint32_t>(g + 8 * r));
-                    }
+            for (int j = 1; j < 16; ++j) w = (i == j) ? bw[j >> 3][(j >> 2) & 1][j & 3] : w;
+            // meta: K offset of the word inside the CTA's K range, B row of the tile
+            const uint32_t koff = o0 + static_cast<uint32_t>(((i >> 2) & 1) * 64 + t * 16 + (i & 3) * 4);
+            my_queue[pos++] = make_uint2(w, (koff << 4) | static_cast<uint32_t>(g + (i & 8)));
+        }
         __syncwarp();
-        // ... and spread (word, A row) units over the lanes, four per lane and pass (loads first)
-        for (int base = 0; base < total * 16; base += 128) {
+        // ... and spread (word, A row) units over the lanes: lane l takes A row l % 16 of entries
+        // (l / 16) + 2 i, four entries per pass (loads first)
+        for (int base = lane >> 4; base < total; base += 8) {
             uint2 e[4];
             uint32_t aw[4];
-            bool on[4];
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
-                const int u = base + i * 32 + lane;
-                on[i] = u < total * 16 && (u & 15) < M;
-                e[i] = on[i] ? my_queue[u >> 4] : make_uint2(0, 0);
-                const int64_t kk = kbeg + (e[i].y >> 4);
-                const uint8_t* p = A + static_cast<int64_t>(u & 15) * lda + kk;
+                const int ei = base + 2 * i;
+                const bool on = ei < total && fix_row_ok;
+                e[i] = on ? my_queue[ei] : make_uint2(0, 0);
+                const uint32_t ko = e[i].y >> 4;
                 aw[i] = 0;
-                if (on[i]) {
-                    if (vec && kk + 4 <= kend) {
-                        aw[i] = __ldg(reinterpret_cast<const uint32_t*>(p));
+                if (on) {
+                    if (vec && kbeg + ko + 4 <= kend) {
+                        aw[i] = __ldg(reinterpret_cast<const uint32_t*>(pa_fix + ko));
                     } else {
                         for (int b4 = 0; b4 < 4; ++b4)
-                            if (kk + b4 < kend) aw[i] |= static_cast<uint32_t>(__ldg(p + b4)) << (8 * b4);
+                            if (kbeg + ko + b4 < kend) aw[i] |= static_cast<uint32_t>(__ldg(pa_fix + ko + b4)) << (8 * b4);
                     }
                 }
             }
 #pragma unroll
             for (int i = 0; i < 4; ++i) {
+                // entries past the list carry a zero word: their correction is zero
                 const int32_t p0 = dp4a_us(aw[i], e[i].x & 0x0000FFFFu, 0), p1 = dp4a_us(aw[i], e[i].x & 0xFFFF0000u, 0);
                 const int32_t fix = sat2_add(p0, p1, 0) - (p0 + p1);
-                if (on[i] && fix != 0) atomicAdd(&corr[(e[i].y & 15u) * MT + ((base + i * 32 + lane) & 15)], fix);
+                if (fix != 0) atomicAdd(&corr[(e[i].y & 15u) * MT + (lane & 15)], fix);
             }
         }
         __syncwarp();
     }
 
+    // this lane's cells of part: the MMA fragment d[nb] = rows {g, g+8} x A rows nb*8 + 2t, +1 (K-phase
+    // plane t of this warp), plus, after a dense chunk, the dense sums of every A row
     if (used_dense) {  // warp-uniform
-        if (lane == 0) *dense_used = 1;  // read after the block-wide barrier below
+        if (lane == 0) atomicOr(dense_mask, 1u << warp);  // read after the block-wide barrier below
 #pragma unroll
         for (int m = 0; m < MT; ++m) {
-            my_part[m] += dacc[0][m];
-            my_part[8 * MT + m] += dacc[1][m];
+            my_part[m] = dacc[0][m];
+            my_part[8 * MT + m] = dacc[1][m];
         }
-    }
-    // this lane's MMA fragment into its own part cells: d[nb] = rows {g, g+8} x A rows nb*8 + 2t, +1
 #pragma unroll
-    for (int nb = 0; nb < NB; ++nb) {
-        const int col = nb * 8 + t * 2;
-        my_part[col] += d[nb][0];
-        my_part[col + 1] += d[nb][1];
-        my_part[8 * MT + col] += d[nb][2];
-        my_part[8 * MT + col + 1] += d[nb][3];
+        for (int nb = 0; nb < NB; ++nb) {
+            const int col = nb * 8 + t * 2;
+            my_part[col] += d[nb][0];
+            my_part[col + 1] += d[nb][1];
+            my_part[8 * MT + col] += d[nb][2];
+            my_part[8 * MT + col + 1] += d[nb][3];
+        }
+    } else {
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) {
+            const int col = nb * 8 + t * 2;
+            *reinterpret_cast<int2*>(my_part + col) = make_int2(d[nb][0], d[nb][1]);
+            *reinterpret_cast<int2*>(my_part + 8 * MT + col) = make_int2(d[nb][2], d[nb][3]);
+        }
     }
     __syncthreads();
     // accumulate == 2: K splits reduced across a thread-block cluster through DSMEM, as in
@@ -953,14 +982,16 @@ __global__ void __launch_bounds__(WARPS * 32, WARPS == 8 ? 2 : 1)
             continue;
         }
         uint32_t s = static_cast<uint32_t>(corr[row * MT + m]);
-        if (*dense_used) {
-#pragma unroll 8
-            for (int w = 0; w < WARPS * 4; ++w) s += static_cast<uint32_t>(part[(w * 16 + row) * MT + m]);
-        } else {
-            // MMA fragments only: A row m sits in K-phase plane (m % 8) / 2 of every warp
+        const unsigned dm = *dense_mask;
+        // a warp without dense chunks holds A row m only in K-phase plane (m % 8) / 2 (its MMA fragment)
 #pragma unroll
-            for (int w = 0; w < WARPS; ++w)
+        for (int w = 0; w < WARPS; ++w) {
+            if (dm & (1u << w)) {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) s += static_cast<uint32_t>(part[((w * 4 + q) * 16 + row) * MT + m]);
+            } else {
                 s += static_cast<uint32_t>(part[((w * 4 + ((m & 7) >> 1)) * 16 + row) * MT + m]);
+            }
         }
         if (xred) {
             xsum[i] = static_cast<int32_t>(s);

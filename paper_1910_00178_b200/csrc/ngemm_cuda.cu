@@ -751,8 +751,8 @@ ngemm_status launch_skinny(const uint8_t* a, int64_t lda, const int8_t* b, int64
     // ~1 us more for TMEM/mbarrier/cluster setup); saturating -> the dp4a load stream (4),
     // which since the pack-saturate step also beats the broadcast kernel (1) on every
     // M > 4, N < 2048 shape (profiles/sweep_r1_skinny_sat_variants.log).
-    // Saturating, 8 < M <= 16: warp MMAs + sparse fix (5) — 1.3-1.5x faster than the dp4a stream on
-    // weight-like B (config 2's sigma = 32: ~0.4 % of the pairs can clamp), 1.3-1.5x slower when
+    // Saturating, 8 < M <= 16: warp MMAs + sparse fix (5) — 1.4-1.8x faster than the dp4a stream on
+    // weight-like B (config 2's sigma = 32: ~0.4 % of the pairs can clamp), 1.1-1.4x slower when
     // most pairs can (uniform int8 B takes its dense branch); NGEMM_SKINNY_VARIANT=4 or a tune-store
     // entry selects the dp4a stream (profiles/r2/skinny_sathyb_r2.log).
     int variant = mode == NGEMM_SAT_EXACT ? 3 : (m > 8 ? 5 : 4);
