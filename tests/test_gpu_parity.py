@@ -868,6 +868,29 @@ def test_fused_requant_epilogue(cuda, oracle, mode):
         assert (pad == 0x55).all(), "requant wrote outside the logical columns"
 
 
+def test_fused_requant_epilogue_pair512_tiles(cuda, oracle, knobs):
+    """The requantising epilogue on the 256 x 512 pair tiles (TC_CFG 9, the configuration AUTO
+    takes for deep K and many waves): TMEM column -> tile column permutation, ragged M / N and a
+    padded output pitch."""
+    import torch
+    knobs.set("TC_CFG", 9)
+    rng = np.random.default_rng(17)
+    for (m, n, k, ldo, zp) in ((300, 1100, 1024, 1104, -2), (513, 512, 384, None, 0)):
+        a = oracle.mat_random_u8(m, k, m + 40)
+        b = oracle.mat_random_i8(n, k, n + 41)
+        scale = (rng.uniform(1.0 / 4000.0, 1.0 / 1000.0, n)).astype(np.float32)
+        bias = rng.integers(-200000, 200000, n, dtype=np.int32)
+        ref = requant_ref(oracle.gemm(a, b, EXACT), scale, bias, zp)
+        ldo = n if ldo is None else ldo
+        out = torch.full((m, ldo), 0x55, dtype=torch.int8, device="cuda")[:, :n]
+        got = api.gemm_device_requant(torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda(),
+                                      torch.from_numpy(scale).cuda(), torch.from_numpy(bias).cuda(), zp, out=out)
+        torch.cuda.synchronize()
+        assert (got.cpu().numpy() == ref).all(), (m, n, k)
+        pad = out.as_strided((m, ldo), (ldo, 1)).cpu().numpy()[:, n:]
+        assert (pad == 0x55).all(), "requant wrote outside the logical columns"
+
+
 def test_stress_repeated_launches_across_streams(cuda, oracle, knobs):
     """Race / sync stress (compute-sanitizer is closed on this pool): the warp-specialised
     mbarrier/TMEM pipelines, the cluster DSMEM reduction, split-K TMA reduce-add and the
