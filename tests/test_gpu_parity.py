@@ -826,6 +826,19 @@ def test_i16_paths_vs_reference_golden(cuda, oracle, golden, path, knobs):
         assert (_dev_gemm_i16(a, b) == oracle.gemm_i16(a, b)).all(), (path, m, n, k)
 
 
+@pytest.mark.gpu
+def test_i16_byte_planes_on_pair512_tiles(cuda, oracle, knobs):
+    """The i16 byte-plane decomposition (shifted stores / TMA reduce-adds of four int8 GEMMs) forced
+    onto the 256 x 512 pair tiles, which AUTO takes for large i16 problems with deep K."""
+    knobs.set("I16_PATH", "tcgen05")
+    knobs.set("TC_CFG", 9)
+    rng = np.random.default_rng(12)
+    for (m, n, k) in [(300, 1100, 512), (513, 520, 777)]:
+        a = rng.integers(-32768, 32768, size=(m, k), dtype=np.int16)
+        b = rng.integers(-32768, 32768, size=(n, k), dtype=np.int16)
+        assert (_dev_gemm_i16(a, b) == oracle.gemm_i16(a, b)).all(), (m, n, k)
+
+
 def requant_ref(c, scale, bias, zp):
     """The fused requantisation's arithmetic in numpy (ngemm_cuda.h): int32 + bias wraps,
     float32 round-to-nearest conversion, one fp32 multiply, rint (half to even), clamp."""
